@@ -1,0 +1,1117 @@
+// C ABI of the B200 state-vector backend (include/qsb.h): contexts, state objects,
+// tapes, and the orchestration of the resident / streaming engines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "qsb_launch.h"
+#include "qsb_plan.h"
+
+using namespace qsb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define QSB_CUDA(call)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (call);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      int _code = (_e == cudaErrorMemoryAllocation) ? QSB_ERR_OOM : QSB_ERR_CUDA;              \
+      return fail(_code, std::string(#call) + ": " + cudaGetErrorString(_e));                  \
+    }                                                                                          \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want ? want : 16);
+    if (e == cudaSuccess) bytes = want ? want : 16;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct PlanDev {
+  StreamPlan plan;
+  DevBuf gates, rops, guard_gates;
+};
+
+}  // namespace
+
+struct qsb_ctx_s {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::vector<cudaEvent_t> pass_events;
+  int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1;
+  DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace;
+  qsb_stats last{};
+};
+
+struct qsb_state_s {
+  qsb_ctx ctx = nullptr;
+  int n = 0;
+  int c64 = 0;
+  DevBuf amps, scratch, tmp;
+};
+
+struct qsb_tape_s {
+  qsb_ctx ctx = nullptr;
+  TapeInfo info;
+  DevBuf d_dev, d_matsrc, d_mats;  // d_mats: literal-only matrix table (no ParamRef angles)
+  std::map<int, std::unique_ptr<PlanDev>> plans;  // key: k * 64 + lowq
+  std::unique_ptr<qsb_tape_s> gates_only;          // static sampling view
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+size_t amp_bytes(int c64) { return c64 ? 8 : 16; }
+
+int tile_qubits(qsb_ctx ctx, int c64) {
+  if (ctx->opt_tile > 0) return (int)std::min<int64_t>(ctx->opt_tile, kMaxTile);
+  return c64 ? 13 : 12;  // 64 KiB of amplitudes per CTA
+}
+int low_qubits(int c64) { return c64 ? 5 : 4; }  // 256-byte contiguous runs
+
+int upload_tape_device(qsb_tape tp) {
+  TapeInfo& t = tp->info;
+  QSB_CUDA(tp->d_dev.ensure(std::max<size_t>(1, t.dev.size()) * sizeof(DevOp)));
+  if (!t.dev.empty())
+    QSB_CUDA(cudaMemcpy(tp->d_dev.p, t.dev.data(), t.dev.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
+  QSB_CUDA(tp->d_matsrc.ensure(std::max<size_t>(1, t.mats.size()) * sizeof(MatSrc)));
+  if (!t.mats.empty())
+    QSB_CUDA(cudaMemcpy(tp->d_matsrc.p, t.mats.data(), t.mats.size() * sizeof(MatSrc), cudaMemcpyHostToDevice));
+  QSB_CUDA(tp->d_mats.ensure(std::max<size_t>(1, t.mats.size()) * 8 * sizeof(double)));
+  if (!t.mats.empty() && !t.has_param_angles) {
+    launch_mats_prep(tp->d_matsrc.as<MatSrc>(), (int)t.mats.size(), nullptr, 0, 1, tp->d_mats.as<double>(),
+                     tp->ctx->stream);
+    QSB_CUDA(cudaGetLastError());
+    QSB_CUDA(cudaStreamSynchronize(tp->ctx->stream));
+  }
+  return QSB_OK;
+}
+
+int get_plan(qsb_tape tp, int k, int lowq, PlanDev** out) {
+  int key = k * 64 + lowq;
+  auto it = tp->plans.find(key);
+  if (it != tp->plans.end()) {
+    *out = it->second.get();
+    return QSB_OK;
+  }
+  auto pd = std::make_unique<PlanDev>();
+  std::string e = build_stream_plan(tp->info, k, lowq, pd->plan);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  StreamPlan& P = pd->plan;
+  QSB_CUDA(pd->gates.ensure(std::max<size_t>(1, P.gates.size()) * sizeof(PassGate)));
+  if (!P.gates.empty())
+    QSB_CUDA(cudaMemcpy(pd->gates.p, P.gates.data(), P.gates.size() * sizeof(PassGate), cudaMemcpyHostToDevice));
+  QSB_CUDA(pd->rops.ensure(std::max<size_t>(1, P.region_ops.size()) * sizeof(DevOp)));
+  if (!P.region_ops.empty())
+    QSB_CUDA(cudaMemcpy(pd->rops.p, P.region_ops.data(), P.region_ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
+  QSB_CUDA(pd->guard_gates.ensure(std::max<size_t>(1, P.guard_gates.size()) * sizeof(int32_t)));
+  QSB_CUDA(cudaMemcpy(pd->guard_gates.p, P.guard_gates.data(), P.guard_gates.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice));
+  *out = pd.get();
+  tp->plans[key] = std::move(pd);
+  return QSB_OK;
+}
+
+// matrix table for a run: shared literal table, or per-slot tables built from params
+int prepare_mats(qsb_tape tp, const double* params_dev, int64_t slots, const double** mats, int64_t* stride) {
+  qsb_ctx ctx = tp->ctx;
+  const TapeInfo& t = tp->info;
+  if (!t.has_param_angles || t.mats.empty()) {
+    *mats = tp->d_mats.as<double>();
+    *stride = 0;
+    return QSB_OK;
+  }
+  size_t per = t.mats.size() * 8;
+  QSB_CUDA(ctx->mats.ensure(per * sizeof(double) * slots));
+  launch_mats_prep(tp->d_matsrc.as<MatSrc>(), (int)t.mats.size(), params_dev, t.nparams, slots,
+                   ctx->mats.as<double>(), ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  *mats = ctx->mats.as<double>();
+  *stride = slots > 1 ? (int64_t)per : 0;
+  return QSB_OK;
+}
+
+int upload_params(qsb_tape tp, const double* params, int64_t rows, const double** out) {
+  qsb_ctx ctx = tp->ctx;
+  int np = tp->info.nparams;
+  if (np == 0) {
+    *out = nullptr;
+    return QSB_OK;
+  }
+  if (!params) return fail(QSB_ERR_ARG, "parameters required");
+  QSB_CUDA(ctx->params.ensure(sizeof(double) * np * rows));
+  QSB_CUDA(cudaMemcpyAsync(ctx->params.p, params, sizeof(double) * np * rows, cudaMemcpyHostToDevice, ctx->stream));
+  *out = ctx->params.as<double>();
+  return QSB_OK;
+}
+
+bool use_resident(qsb_ctx ctx, const TapeInfo& t, int c64) {
+  if (ctx->opt_engine == 0) return true;
+  if (ctx->opt_engine == 1) return false;
+  int lim = ctx->opt_resident_max >= 0 ? (int)ctx->opt_resident_max : resident_max_qubits(c64);
+  lim = std::min(lim, resident_max_qubits(c64));
+  return t.n <= lim && t.nwords <= kResMaxWords;
+}
+
+struct RunTimer {
+  qsb_ctx ctx;
+  explicit RunTimer(qsb_ctx c) : ctx(c) { cudaEventRecord(ctx->ev_a, ctx->stream); }
+  float stop() {
+    cudaEventRecord(ctx->ev_b, ctx->stream);
+    cudaEventSynchronize(ctx->ev_b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b);
+    return ms;
+  }
+};
+
+// Executes the streaming plan for `slots` states already allocated at `state`.
+// Control blocks / bits / guards / partials live in the context scratch.
+struct StreamRun {
+  qsb_tape tp;
+  PlanDev* pd;
+  int c64;
+  int64_t slots;
+  void* state;
+  const double* mats;
+  int64_t mat_stride;
+  uint64_t seed;
+  int64_t shot_begin;
+  const double* predrawn;
+  int predrawn_stride;
+  int64_t predrawn_slot0;
+  int64_t* trace;
+  int max_trace;
+  int32_t* ntrace;
+  const uint64_t* rng_init = nullptr;
+  uint64_t final_clear = 0;
+  int final_consumed = 0;
+  double pass_bytes = 0;
+  int64_t passes = 0, decides = 0, launches = 0;
+  std::vector<std::pair<int, int>> pass_event_idx;
+};
+
+int alloc_stream_scratch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, int64_t slots) {
+  QSB_CUDA(ctx->ctl.ensure(sizeof(TrajCtl) * slots));
+  QSB_CUDA(ctx->bits.ensure(sizeof(uint64_t) * t.nwords * slots));
+  QSB_CUDA(ctx->guards.ensure(sizeof(uint32_t) * t.gwords * slots));
+  int64_t pstride = ((int64_t)1 << P.ntiles_log2) * P.max_local_bins;
+  QSB_CUDA(ctx->partial.ensure(sizeof(double) * pstride * slots));
+  return QSB_OK;
+}
+
+int run_stream(qsb_ctx ctx, StreamRun& r) {
+  const TapeInfo& t = r.tp->info;
+  const StreamPlan& P = r.pd->plan;
+  int rc = alloc_stream_scratch(ctx, t, P, r.slots);
+  if (rc) return rc;
+  StreamArgs a{};
+  a.state = r.state;
+  a.n = t.n;
+  a.c64 = r.c64;
+  a.gates = r.pd->gates.as<PassGate>();
+  a.mats = r.mats;
+  a.mat_stride = r.mat_stride;
+  a.ctl = ctx->ctl.as<TrajCtl>();
+  a.bits = ctx->bits.as<uint64_t>();
+  a.nwords = t.nwords;
+  a.gwords = t.gwords;
+  a.guards = ctx->guards.as<uint32_t>();
+  a.partial = ctx->partial.as<double>();
+  a.partial_stride = ((int64_t)1 << P.ntiles_log2) * P.max_local_bins;
+  a.slots = r.slots;
+  a.region_ops = r.pd->rops.as<DevOp>();
+  a.predrawn = r.predrawn;
+  a.predrawn_stride = r.predrawn_stride;
+  a.ntiles_log2 = P.ntiles_log2;
+  a.predrawn_slot0 = r.predrawn_slot0;
+  a.tie_count = ctx->counters.as<unsigned long long>();
+  a.trace_out = r.trace;
+  a.max_trace = r.max_trace;
+  a.ntrace_out = r.ntrace;
+  launch_ctl_init(a.ctl, a.bits, t.nwords, a.guards, t.gwords, r.slots, r.seed, r.shot_begin, r.rng_init, ctx->stream);
+  r.launches++;
+  if (P.passes.empty()) {
+    launch_init_zero(r.c64, r.state, t.n, r.slots, ctx->stream);
+    r.launches++;
+  }
+  size_t need_events = 2 * P.passes.size();
+  while (ctx->pass_events.size() < need_events) {
+    cudaEvent_t e;
+    QSB_CUDA(cudaEventCreate(&e));
+    ctx->pass_events.push_back(e);
+  }
+  uint64_t acc = 0;
+  int consumed = 0;
+  const double state_bytes = (double)amp_bytes(r.c64) * (double)((int64_t)1 << t.n) * (double)r.slots;
+  for (const Step& s : P.steps) {
+    if (s.type == 0) {
+      const PassDesc& pd = P.passes[s.index];
+      cudaEventRecord(ctx->pass_events[2 * s.index], ctx->stream);
+      QSB_CUDA(launch_pass(a, pd, ctx->stream));
+      cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
+      r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
+      r.passes++;
+      r.launches++;
+      acc |= pd.smask;
+      if (pd.prologue) consumed = 1;
+    } else {
+      const RegionDesc& rd = P.regions[s.index];
+      QSB_CUDA(launch_decide(a, rd, ctx->stream));
+      r.decides++;
+      r.launches++;
+      acc = 0;
+      consumed = 0;
+    }
+  }
+  r.final_clear = acc;
+  r.final_consumed = consumed;
+  launch_count_gates(a, r.pd->guard_gates.as<int32_t>(), t.nguards, P.unguarded_gates,
+                     ctx->counters.as<unsigned long long>() + 1, ctx->stream);
+  r.launches++;
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
+double pass_ms_sum(qsb_ctx ctx, size_t npasses) {
+  double tot = 0;
+  for (size_t i = 0; i < npasses; ++i) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ctx->pass_events[2 * i], ctx->pass_events[2 * i + 1]) == cudaSuccess) tot += ms;
+  }
+  return tot;
+}
+
+int64_t pick_batch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, int c64, int64_t count) {
+  if (ctx->opt_batch > 0) return std::min<int64_t>(ctx->opt_batch, count);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  // already-held scratch counts as available
+  size_t held = ctx->state.bytes + ctx->partial.bytes;
+  double per = (double)amp_bytes(c64) * std::ldexp(1.0, t.n) +
+               8.0 * std::ldexp(1.0, P.ntiles_log2) * P.max_local_bins + sizeof(TrajCtl) + 8.0 * t.nwords +
+               4.0 * t.gwords;
+  double budget = 0.85 * (double)(free_b + held) - 256.0 * 1024 * 1024;
+  int64_t b = (int64_t)(budget / per);
+  b = std::max<int64_t>(1, std::min<int64_t>(b, 65535));
+  return std::min<int64_t>(b, count);
+}
+
+int finish_stats(qsb_ctx ctx, float total_ms, double pass_ms, double pass_bytes, int64_t passes, int64_t decides,
+                 int64_t launches, int engine, int k) {
+  unsigned long long cnt[2] = {0, 0};
+  QSB_CUDA(cudaMemcpy(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+  ctx->last.kernel_launches = launches;
+  ctx->last.passes = passes;
+  ctx->last.decides = decides;
+  ctx->last.pass_ms = pass_ms;
+  ctx->last.total_ms = total_ms;
+  ctx->last.pass_bytes = pass_bytes;
+  ctx->last.gate_updates = (int64_t)cnt[1];
+  ctx->last.tie_band = (int64_t)cnt[0];
+  ctx->last.engine = engine;
+  ctx->last.tile_qubits = k;
+  return QSB_OK;
+}
+
+int check_sticky() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(QSB_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+  return QSB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* qsb_last_error(void) { return g_err.c_str(); }
+int32_t qsb_abi_version(void) { return QSB_ABI_VERSION; }
+
+int32_t qsb_device_count(int32_t* count) {
+  int c = 0;
+  QSB_CUDA(cudaGetDeviceCount(&c));
+  *count = c;
+  return QSB_OK;
+}
+
+int32_t qsb_ctx_create(int32_t device, qsb_ctx* out) {
+  if (!out) return fail(QSB_ERR_ARG, "null out");
+  int cnt = 0;
+  QSB_CUDA(cudaGetDeviceCount(&cnt));
+  if (device < 0 || device >= cnt) return fail(QSB_ERR_ARG, "device index out of range");
+  DeviceGuard g(device);
+  QSB_CUDA(cudaSetDevice(device));
+  auto* c = new qsb_ctx_s();
+  c->device = device;
+  cudaDeviceProp prop;
+  QSB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) {
+    delete c;
+    return fail(QSB_ERR_UNSUPPORTED, std::string("needs an sm_100 (B200) device, found ") + prop.name);
+  }
+  c->num_sms = prop.multiProcessorCount;
+  QSB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  QSB_CUDA(cudaEventCreate(&c->ev_a));
+  QSB_CUDA(cudaEventCreate(&c->ev_b));
+  QSB_CUDA(c->counters.ensure(64));
+  *out = c;
+  return QSB_OK;
+}
+
+int32_t qsb_ctx_destroy(qsb_ctx ctx) {
+  if (!ctx) return QSB_OK;
+  DeviceGuard g(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->state, &ctx->partial, &ctx->ctl, &ctx->bits, &ctx->guards, &ctx->mats, &ctx->params,
+                    &ctx->predrawn, &ctx->status, &ctx->counters, &ctx->misc, &ctx->misc2, &ctx->trace})
+    b->release();
+  for (auto e : ctx->pass_events) cudaEventDestroy(e);
+  cudaEventDestroy(ctx->ev_a);
+  cudaEventDestroy(ctx->ev_b);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return QSB_OK;
+}
+
+int32_t qsb_ctx_synchronize(qsb_ctx ctx) {
+  DeviceGuard g(ctx->device);
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}
+
+int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
+  std::string k = key ? key : "";
+  if (k == "tile_qubits") ctx->opt_tile = value;
+  else if (k == "batch") ctx->opt_batch = value;
+  else if (k == "resident_max_qubits") ctx->opt_resident_max = value;
+  else if (k == "engine") ctx->opt_engine = value;  // -1 auto, 0 resident, 1 streaming
+  else if (k == "release_scratch") {
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->state, &ctx->partial, &ctx->ctl, &ctx->bits, &ctx->guards, &ctx->mats, &ctx->params,
+                      &ctx->predrawn, &ctx->status, &ctx->misc, &ctx->misc2, &ctx->trace})
+      b->release();
+  } else return fail(QSB_ERR_ARG, "unknown option " + k);
+  return QSB_OK;
+}
+
+int32_t qsb_ctx_last_stats(qsb_ctx ctx, qsb_stats* out) {
+  *out = ctx->last;
+  return QSB_OK;
+}
+
+// ---- states ------------------------------------------------------------------
+int32_t qsb_state_create(qsb_ctx ctx, int32_t nqubits, int32_t precision, qsb_state* out) {
+  if (nqubits < 0 || nqubits > 40) return fail(QSB_ERR_UNSUPPORTED, "qubit count outside [0, 40] for one state");
+  DeviceGuard g(ctx->device);
+  auto* s = new qsb_state_s();
+  s->ctx = ctx;
+  s->n = nqubits;
+  s->c64 = precision == QSB_C64 ? 1 : 0;
+  cudaError_t e = s->amps.ensure(amp_bytes(s->c64) << nqubits);
+  if (e == cudaSuccess) e = s->scratch.ensure(sizeof(double) * (prob_scratch_len(nqubits) + 8));
+  if (e != cudaSuccess) {
+    s->amps.release();
+    s->scratch.release();
+    delete s;
+    return fail(e == cudaErrorMemoryAllocation ? QSB_ERR_OOM : QSB_ERR_CUDA, cudaGetErrorString(e));
+  }
+  launch_init_zero(s->c64, s->amps.p, nqubits, 1, ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  *out = s;
+  return QSB_OK;
+}
+
+int32_t qsb_state_destroy(qsb_state st) {
+  if (!st) return QSB_OK;
+  DeviceGuard g(st->ctx->device);
+  cudaStreamSynchronize(st->ctx->stream);
+  st->amps.release();
+  st->scratch.release();
+  st->tmp.release();
+  delete st;
+  return QSB_OK;
+}
+
+int32_t qsb_state_set(qsb_state st, const double* amps) {
+  DeviceGuard g(st->ctx->device);
+  size_t N = (size_t)1 << st->n;
+  if (!st->c64) {
+    QSB_CUDA(cudaMemcpyAsync(st->amps.p, amps, 16 * N, cudaMemcpyHostToDevice, st->ctx->stream));
+  } else {
+    QSB_CUDA(st->tmp.ensure(16 * N));
+    QSB_CUDA(cudaMemcpyAsync(st->tmp.p, amps, 16 * N, cudaMemcpyHostToDevice, st->ctx->stream));
+    launch_c128_to_c64(st->tmp.as<double>(), st->amps.as<float>(), (int64_t)N, st->ctx->stream);
+  }
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  return QSB_OK;
+}
+
+int32_t qsb_state_get(qsb_state st, double* amps) {
+  DeviceGuard g(st->ctx->device);
+  size_t N = (size_t)1 << st->n;
+  if (!st->c64) {
+    QSB_CUDA(cudaMemcpyAsync(amps, st->amps.p, 16 * N, cudaMemcpyDeviceToHost, st->ctx->stream));
+  } else {
+    QSB_CUDA(st->tmp.ensure(16 * N));
+    launch_c64_to_c128(st->amps.as<float>(), st->tmp.as<double>(), (int64_t)N, st->ctx->stream);
+    QSB_CUDA(cudaMemcpyAsync(amps, st->tmp.p, 16 * N, cudaMemcpyDeviceToHost, st->ctx->stream));
+  }
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  return QSB_OK;
+}
+
+int32_t qsb_state_copy(qsb_state dst, qsb_state src) {
+  if (dst->n != src->n || dst->c64 != src->c64) return fail(QSB_ERR_DIMENSION, "state shape / precision mismatch");
+  DeviceGuard g(dst->ctx->device);
+  QSB_CUDA(cudaMemcpyAsync(dst->amps.p, src->amps.p, amp_bytes(src->c64) << src->n, cudaMemcpyDeviceToDevice,
+                           dst->ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(dst->ctx->stream));
+  return QSB_OK;
+}
+
+int32_t qsb_state_norm(qsb_state st, double* out) {
+  DeviceGuard g(st->ctx->device);
+  double* sc = st->scratch.as<double>();
+  launch_prob(st->c64, st->amps.p, st->n, -1, sc + 8, sc, st->ctx->stream);
+  double v = 0;
+  QSB_CUDA(cudaMemcpyAsync(&v, sc, sizeof(double), cudaMemcpyDeviceToHost, st->ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  *out = std::sqrt(v);
+  return QSB_OK;
+}
+
+int32_t qsb_state_device_ptr(qsb_state st, void** out) {
+  *out = st->amps.p;
+  return QSB_OK;
+}
+
+int32_t qsb_apply_gate(qsb_state st, const qsb_op* op, const double* params, int32_t nparams) {
+  if (!op || op->kind != QSB_OP_GATE) return fail(QSB_ERR_ARG, "not a gate op");
+  TapeInfo ti;
+  std::string e = analyze_tape(op, 1, st->n, 0, nparams, ti);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  DeviceGuard g(st->ctx->device);
+  const DevOp& d = ti.dev[0];
+  double m[8];
+  if (ti.mats[0].has_matrix) {
+    std::memcpy(m, ti.mats[0].mat, sizeof(m));
+  } else {  // ParamRef / literal angles: build on the device, bring the 2x2 back
+    double* sc = st->scratch.as<double>();
+    QSB_CUDA(st->tmp.ensure(sizeof(MatSrc) + sizeof(double) * (nparams + 1)));
+    char* tb = st->tmp.as<char>();
+    QSB_CUDA(cudaMemcpyAsync(tb, &ti.mats[0], sizeof(MatSrc), cudaMemcpyHostToDevice, st->ctx->stream));
+    if (nparams > 0)
+      QSB_CUDA(cudaMemcpyAsync(tb + sizeof(MatSrc), params, sizeof(double) * nparams, cudaMemcpyHostToDevice,
+                               st->ctx->stream));
+    launch_mats_prep(reinterpret_cast<MatSrc*>(tb), 1, nparams > 0 ? reinterpret_cast<double*>(tb + sizeof(MatSrc)) : nullptr,
+                     nparams, 1, sc, st->ctx->stream);
+    QSB_CUDA(cudaMemcpyAsync(m, sc, sizeof(m), cudaMemcpyDeviceToHost, st->ctx->stream));
+    QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  }
+  if (d.gclass == GC_SWAP) launch_apply_swap(st->c64, st->amps.p, st->n, d.t0, d.t1, d.cm, d.cv, st->ctx->stream);
+  else launch_apply_1q(st->c64, st->amps.p, st->n, d.t0, d.cm, d.cv, d.gclass, m, st->ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
+int32_t qsb_measure(qsb_state st, int32_t qubit, double u, int32_t* outcome, double* p1_out) {
+  if (qubit < 0 || qubit >= st->n) return fail(QSB_ERR_ARG, "qubit out of range");
+  DeviceGuard g(st->ctx->device);
+  double* sc = st->scratch.as<double>();
+  launch_prob(st->c64, st->amps.p, st->n, qubit, sc + 8, sc, st->ctx->stream);
+  double p1 = 0;
+  QSB_CUDA(cudaMemcpyAsync(&p1, sc, sizeof(double), cudaMemcpyDeviceToHost, st->ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  int o = u < p1 ? 1 : 0;
+  double pout = o ? p1 : 1.0 - p1;
+  if (p1_out) *p1_out = p1;
+  if (outcome) *outcome = o;
+  if (pout < 1e-15) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "selected measurement branch %d on qubit %d has probability %.17g", o, qubit, pout);
+    return fail(QSB_ERR_DEGENERATE, buf);
+  }
+  launch_collapse(st->c64, st->amps.p, st->n, qubit, o, 1.0 / std::sqrt(pout), 0, st->ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
+int32_t qsb_reset(qsb_state st, int32_t qubit, double u, int32_t* outcome) {
+  if (qubit < 0 || qubit >= st->n) return fail(QSB_ERR_ARG, "qubit out of range");
+  DeviceGuard g(st->ctx->device);
+  double* sc = st->scratch.as<double>();
+  launch_prob(st->c64, st->amps.p, st->n, qubit, sc + 8, sc, st->ctx->stream);
+  double p1 = 0;
+  QSB_CUDA(cudaMemcpyAsync(&p1, sc, sizeof(double), cudaMemcpyDeviceToHost, st->ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  int o = u < p1 ? 1 : 0;
+  double pout = o ? p1 : 1.0 - p1;
+  if (outcome) *outcome = o;
+  if (pout < 1e-15) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "selected measurement branch %d on qubit %d has probability %.17g", o, qubit, pout);
+    return fail(QSB_ERR_DEGENERATE, buf);
+  }
+  launch_collapse(st->c64, st->amps.p, st->n, qubit, o, 1.0 / std::sqrt(pout), 1, st->ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
+}  // extern "C"
+
+// ---- Pauli expectation (shared by qsb_expval_pauli and qsb_observe) -----------------
+namespace {
+
+int expval_terms(qsb_ctx ctx, int c64, const void* amps, int n, int64_t slots, const uint64_t* xm,
+                 const uint64_t* zm, const int32_t* ny, int nterm, double* out_host /*[slots][nterm]*/) {
+  std::map<uint64_t, std::vector<int>> groups;
+  for (int t = 0; t < nterm; ++t) groups[xm[t]].push_back(t);
+  int blocks = expval_blocks(n);
+  QSB_CUDA(ctx->misc.ensure(sizeof(double) * blocks * nterm * slots));
+  QSB_CUDA(ctx->misc2.ensure((sizeof(double) + sizeof(uint64_t) + sizeof(int32_t)) * nterm * slots + 64));
+  // term order for the kernels: grouped, then mapped back
+  std::vector<int> order;
+  for (auto& kv : groups)
+    for (int t : kv.second) order.push_back(t);
+  std::vector<uint64_t> gx(nterm);
+  std::vector<int32_t> gny(nterm);
+  for (int i = 0; i < nterm; ++i) {
+    gx[i] = xm[order[i]];
+    gny[i] = ny[order[i]];
+  }
+  int pos = 0;
+  for (auto& kv : groups) {
+    const std::vector<int>& ts = kv.second;
+    for (size_t c = 0; c < ts.size(); c += 8) {
+      PauliGroup g{};
+      g.xmask = kv.first;
+      g.nterm = (int)std::min<size_t>(8, ts.size() - c);
+      g.term0 = pos;
+      for (int j = 0; j < g.nterm; ++j) {
+        g.zy[j] = zm[ts[c + j]];
+        g.ny[j] = ny[ts[c + j]];
+      }
+      launch_expval_group(c64, amps, n, slots, g, ctx->misc.as<double>(), nterm, ctx->stream);
+      pos += g.nterm;
+    }
+  }
+  char* base = ctx->misc2.as<char>();
+  double* d_out = reinterpret_cast<double*>(base);
+  uint64_t* d_x = reinterpret_cast<uint64_t*>(base + sizeof(double) * nterm * slots);
+  int32_t* d_ny = reinterpret_cast<int32_t*>(d_x + nterm);
+  QSB_CUDA(cudaMemcpyAsync(d_x, gx.data(), sizeof(uint64_t) * nterm, cudaMemcpyHostToDevice, ctx->stream));
+  QSB_CUDA(cudaMemcpyAsync(d_ny, gny.data(), sizeof(int32_t) * nterm, cudaMemcpyHostToDevice, ctx->stream));
+  launch_expval_finish(ctx->misc.as<double>(), slots, nterm, blocks, d_x, d_ny, d_out, ctx->stream);
+  std::vector<double> tmp((size_t)nterm * slots);
+  QSB_CUDA(cudaMemcpyAsync(tmp.data(), d_out, sizeof(double) * nterm * slots, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t s = 0; s < slots; ++s)
+    for (int i = 0; i < nterm; ++i) out_host[s * nterm + order[i]] = tmp[s * nterm + i];
+  return QSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t qsb_expval_pauli(qsb_state st, uint64_t xmask, uint64_t zmask, int32_t ny, double* out) {
+  uint64_t qm = st->n >= 64 ? ~0ull : ((1ull << st->n) - 1);
+  if ((xmask & ~qm) || (zmask & ~qm)) return fail(QSB_ERR_BAD_PAULI, "pauli mask outside the register");
+  DeviceGuard g(st->ctx->device);
+  return expval_terms(st->ctx, st->c64, st->amps.p, st->n, 1, &xmask, &zmask, &ny, 1, out);
+}
+
+// ---- tapes ------------------------------------------------------------------
+int32_t qsb_tape_create(qsb_ctx ctx, const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                        qsb_tape* out) {
+  auto* tp = new qsb_tape_s();
+  tp->ctx = ctx;
+  std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, tp->info);
+  if (!e.empty()) {
+    delete tp;
+    return fail(QSB_ERR_ARG, e);
+  }
+  DeviceGuard g(ctx->device);
+  int rc = upload_tape_device(tp);
+  if (rc) {
+    delete tp;
+    return rc;
+  }
+  // gates-only view for static sampling (_gates_only_state, sim.py:338-343)
+  std::vector<qsb_op> gops;
+  for (int i = 0; i < nops; ++i)
+    if (ops[i].kind == QSB_OP_GATE) gops.push_back(ops[i]);
+  if ((int)gops.size() != nops) {
+    auto* go = new qsb_tape_s();
+    go->ctx = ctx;
+    analyze_tape(gops.data(), (int)gops.size(), nqubits, nbits, nparams, go->info);
+    rc = upload_tape_device(go);
+    if (rc) {
+      delete go;
+      delete tp;
+      return rc;
+    }
+    tp->gates_only.reset(go);
+  }
+  *out = tp;
+  return QSB_OK;
+}
+
+int32_t qsb_tape_destroy(qsb_tape tp) {
+  if (!tp) return QSB_OK;
+  DeviceGuard g(tp->ctx->device);
+  cudaStreamSynchronize(tp->ctx->stream);
+  std::vector<qsb_tape> all = {tp};
+  if (tp->gates_only) all.push_back(tp->gates_only.get());
+  for (qsb_tape t : all) {
+    t->d_dev.release();
+    t->d_matsrc.release();
+    t->d_mats.release();
+    for (auto& kv : t->plans) {
+      kv.second->gates.release();
+      kv.second->rops.release();
+      kv.second->guard_gates.release();
+    }
+  }
+  delete tp;
+  return QSB_OK;
+}
+
+int32_t qsb_tape_is_dynamic(qsb_tape tp, int32_t* out) {
+  *out = tp->info.needs_trajectories ? 1 : 0;
+  return QSB_OK;
+}
+
+int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
+                                int64_t shot_begin, int64_t shot_count, const double* predrawn,
+                                int32_t predrawn_stride, uint64_t* bits_out, int32_t* shot_status) {
+  if (shot_count < 1) return fail(QSB_ERR_SIM, "shots must be >= 1");
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  const TapeInfo& t = tp->info;
+  const int c64 = precision == QSB_C64 ? 1 : 0;
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  RunTimer timer(ctx);
+  const double* d_params = nullptr;
+  int rc = upload_params(tp, params, 1, &d_params);
+  if (rc) return rc;
+  const double* mats;
+  int64_t mstride;
+  rc = prepare_mats(tp, d_params, 1, &mats, &mstride);
+  if (rc) return rc;
+  const double* d_pre = nullptr;
+  if (predrawn) {
+    if (predrawn_stride < 0) return fail(QSB_ERR_ARG, "bad predrawn stride");
+    QSB_CUDA(ctx->predrawn.ensure(sizeof(double) * std::max<int64_t>(1, (int64_t)predrawn_stride * shot_count)));
+    QSB_CUDA(cudaMemcpyAsync(ctx->predrawn.p, predrawn, sizeof(double) * predrawn_stride * shot_count,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    d_pre = ctx->predrawn.as<double>();
+  }
+  std::vector<int32_t> status((size_t)shot_count, 0);
+  if (use_resident(ctx, t, c64)) {
+    QSB_CUDA(ctx->bits.ensure(sizeof(uint64_t) * t.nwords * shot_count));
+    QSB_CUDA(ctx->status.ensure(sizeof(int32_t) * shot_count));
+    ResidentArgs a{};
+    a.ops = tp->d_dev.as<DevOp>();
+    a.nops = (int)t.dev.size();
+    a.n = t.n;
+    a.nwords = t.nwords;
+    a.predrawn_stride = predrawn_stride;
+    a.mats = mats;
+    a.mat_stride = 0;
+    a.seed = seed;
+    a.shot_begin = shot_begin;
+    a.count = shot_count;
+    a.predrawn = d_pre;
+    a.bits_out = ctx->bits.as<uint64_t>();
+    a.status_out = ctx->status.as<int32_t>();
+    a.tie_count = ctx->counters.as<unsigned long long>();
+    a.gate_count = ctx->counters.as<unsigned long long>() + 1;
+    a.c64 = c64;
+    QSB_CUDA(launch_resident(a, ctx->num_sms, ctx->stream));
+    QSB_CUDA(cudaMemcpyAsync(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    QSB_CUDA(cudaMemcpyAsync(status.data(), ctx->status.p, sizeof(int32_t) * shot_count, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    float ms = timer.stop();
+    rc = check_sticky();
+    if (rc) return rc;
+    finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
+  } else {
+    PlanDev* pd;
+    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+    if (rc) return rc;
+    int64_t B = pick_batch(ctx, t, pd->plan, c64, shot_count);
+    QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
+    double pass_ms = 0, pass_bytes = 0;
+    int64_t passes = 0, decides = 0, launches = 0;
+    for (int64_t off = 0; off < shot_count; off += B) {
+      int64_t b = std::min(B, shot_count - off);
+      StreamRun r{tp, pd, c64, b, ctx->state.p, mats, mstride, seed, shot_begin + off, d_pre, predrawn_stride, off,
+                  nullptr, 0, nullptr};
+      rc = run_stream(ctx, r);
+      if (rc) return rc;
+      QSB_CUDA(cudaMemcpyAsync(bits_out + off * t.nwords, ctx->bits.p, sizeof(uint64_t) * t.nwords * b,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      std::vector<TrajCtl> ctl((size_t)b);
+      QSB_CUDA(cudaMemcpyAsync(ctl.data(), ctx->ctl.p, sizeof(TrajCtl) * b, cudaMemcpyDeviceToHost, ctx->stream));
+      QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t i = 0; i < b; ++i) status[off + i] = ctl[i].status;
+      pass_ms += pass_ms_sum(ctx, pd->plan.passes.size());
+      pass_bytes += r.pass_bytes;
+      passes += r.passes;
+      decides += r.decides;
+      launches += r.launches;
+    }
+    float ms = timer.stop();
+    rc = check_sticky();
+    if (rc) return rc;
+    finish_stats(ctx, ms, pass_ms, pass_bytes, passes, decides, launches, 1, pd->plan.k);
+  }
+  int worst = QSB_OK;
+  for (int64_t i = 0; i < shot_count; ++i) {
+    if (shot_status) shot_status[i] = status[i];
+    if (status[i] != QSB_OK && worst == QSB_OK) worst = status[i];
+  }
+  if (worst == QSB_ERR_DEGENERATE) return fail(worst, "selected measurement branch has probability < 1e-15");
+  if (worst == QSB_ERR_PREDRAWN) return fail(worst, "pre-drawn uniform stream exhausted");
+  if (worst != QSB_OK) return fail(worst, "trajectory failed");
+  return QSB_OK;
+}
+
+int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params, uint64_t* rng_state, uint64_t seed,
+                           int64_t shot, const double* predrawn, int32_t npredrawn, uint64_t* bits_out,
+                           qsb_state state_out, int64_t* trace_out, int32_t max_trace, int32_t* ntrace,
+                           int32_t* ndraws) {
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  const TapeInfo& t = tp->info;
+  const int c64 = precision == QSB_C64 ? 1 : 0;
+  if (state_out && (state_out->n != t.n || state_out->c64 != c64))
+    return fail(QSB_ERR_DIMENSION, "state_out shape / precision mismatch");
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  RunTimer timer(ctx);
+  const double* d_params = nullptr;
+  int rc = upload_params(tp, params, 1, &d_params);
+  if (rc) return rc;
+  const double* mats;
+  int64_t mstride;
+  rc = prepare_mats(tp, d_params, 1, &mats, &mstride);
+  if (rc) return rc;
+  const double* d_pre = nullptr;
+  if (predrawn) {
+    QSB_CUDA(ctx->predrawn.ensure(sizeof(double) * std::max(1, npredrawn)));
+    if (npredrawn > 0)
+      QSB_CUDA(cudaMemcpyAsync(ctx->predrawn.p, predrawn, sizeof(double) * npredrawn, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    d_pre = ctx->predrawn.as<double>();
+  }
+  int64_t* d_trace = nullptr;
+  int32_t* d_ntrace = nullptr;
+  size_t trace_bytes = trace_out ? sizeof(int64_t) * (size_t)std::max(1, max_trace) * (2 + t.nwords) : 0;
+  QSB_CUDA(ctx->trace.ensure(trace_bytes + 128));
+  d_ntrace = reinterpret_cast<int32_t*>(ctx->trace.as<char>());
+  int32_t* d_draws = d_ntrace + 1;
+  uint64_t* d_rng = reinterpret_cast<uint64_t*>(ctx->trace.as<char>() + 64);
+  QSB_CUDA(cudaMemsetAsync(d_ntrace, 0, 2 * sizeof(int32_t), ctx->stream));
+  if (rng_state)
+    QSB_CUDA(cudaMemcpyAsync(d_rng, rng_state, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  if (trace_out) d_trace = reinterpret_cast<int64_t*>(ctx->trace.as<char>() + 128);
+  int32_t status = 0;
+  if (use_resident(ctx, t, c64)) {
+    QSB_CUDA(ctx->bits.ensure(sizeof(uint64_t) * t.nwords));
+    QSB_CUDA(ctx->status.ensure(sizeof(int32_t)));
+    ResidentArgs a{};
+    a.ops = tp->d_dev.as<DevOp>();
+    a.nops = (int)t.dev.size();
+    a.n = t.n;
+    a.nwords = t.nwords;
+    a.predrawn_stride = npredrawn;
+    a.mats = mats;
+    a.seed = seed;
+    a.shot_begin = shot;
+    a.count = 1;
+    a.predrawn = d_pre;
+    a.bits_out = ctx->bits.as<uint64_t>();
+    a.status_out = ctx->status.as<int32_t>();
+    a.state_out = state_out ? state_out->amps.p : nullptr;
+    a.trace_out = d_trace;
+    a.max_trace = max_trace;
+    a.ntrace_out = d_ntrace;
+    a.tie_count = ctx->counters.as<unsigned long long>();
+    a.gate_count = ctx->counters.as<unsigned long long>() + 1;
+    a.rng_init = rng_state ? d_rng : nullptr;
+    a.rng_final = d_rng;
+    a.draws_out = d_draws;
+    a.c64 = c64;
+    QSB_CUDA(launch_resident(a, ctx->num_sms, ctx->stream));
+    QSB_CUDA(cudaMemcpyAsync(&status, ctx->status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    float ms = timer.stop();
+    rc = check_sticky();
+    if (rc) return rc;
+    finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
+  } else {
+    PlanDev* pd;
+    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+    if (rc) return rc;
+    QSB_CUDA(ctx->state.ensure(amp_bytes(c64) << t.n));
+    StreamRun r{tp, pd, c64, 1, ctx->state.p, mats, mstride, seed, shot, d_pre, npredrawn, 0, d_trace, max_trace,
+                d_ntrace};
+    r.rng_init = rng_state ? d_rng : nullptr;
+    rc = run_stream(ctx, r);
+    if (rc) return rc;
+    StreamArgs a{};
+    a.state = ctx->state.p;
+    a.n = t.n;
+    a.c64 = c64;
+    a.ctl = ctx->ctl.as<TrajCtl>();
+    if (state_out) launch_finalize(a, state_out->amps.p, r.final_clear, r.final_consumed, ctx->stream);
+    TrajCtl c;
+    QSB_CUDA(cudaMemcpyAsync(&c, ctx->ctl.p, sizeof(TrajCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    float ms = timer.stop();
+    rc = check_sticky();
+    if (rc) return rc;
+    status = c.status;
+    QSB_CUDA(cudaMemcpy(d_rng, c.rng, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    QSB_CUDA(cudaMemcpy(d_draws, &c.draws, sizeof(int32_t), cudaMemcpyHostToDevice));
+    finish_stats(ctx, ms, pass_ms_sum(ctx, pd->plan.passes.size()), r.pass_bytes, r.passes, r.decides, r.launches + 1,
+                 1, pd->plan.k);
+  }
+  QSB_CUDA(cudaMemcpy(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords, cudaMemcpyDeviceToHost));
+  int32_t nt2[2] = {0, 0};
+  QSB_CUDA(cudaMemcpy(nt2, d_ntrace, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  int32_t nt = nt2[0];
+  if (ntrace) *ntrace = nt;
+  if (ndraws) *ndraws = nt2[1];
+  if (rng_state) QSB_CUDA(cudaMemcpy(rng_state, d_rng, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (trace_out && nt > 0)
+    QSB_CUDA(cudaMemcpy(trace_out, d_trace, sizeof(int64_t) * std::min(nt, max_trace) * (2 + t.nwords),
+                        cudaMemcpyDeviceToHost));
+  if (status == QSB_ERR_DEGENERATE) return fail(status, "selected measurement branch has probability < 1e-15");
+  if (status == QSB_ERR_PREDRAWN) return fail(status, "pre-drawn uniform stream exhausted");
+  if (status != QSB_OK) return fail(status, "trajectory failed");
+  return QSB_OK;
+}
+
+int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
+  const TapeInfo& t = tp->info;
+  if (t.top_level_dynamic) return fail(QSB_ERR_DYNAMIC, "Measure/CondBlock/Reset requires trajectory sampling; use sample()");
+  if (out->n != t.n) return fail(QSB_ERR_DIMENSION, "output state has the wrong qubit count");
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  const int c64 = out->c64;
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  RunTimer timer(ctx);
+  const double* d_params = nullptr;
+  int rc = upload_params(tp, params, 1, &d_params);
+  if (rc) return rc;
+  const double* mats;
+  int64_t mstride;
+  rc = prepare_mats(tp, d_params, 1, &mats, &mstride);
+  if (rc) return rc;
+  if (use_resident(ctx, t, c64)) {
+    QSB_CUDA(ctx->bits.ensure(sizeof(uint64_t) * t.nwords));
+    QSB_CUDA(ctx->status.ensure(sizeof(int32_t)));
+    ResidentArgs a{};
+    a.ops = tp->d_dev.as<DevOp>();
+    a.nops = (int)t.dev.size();
+    a.n = t.n;
+    a.nwords = t.nwords;
+    a.mats = mats;
+    a.count = 1;
+    a.bits_out = ctx->bits.as<uint64_t>();
+    a.status_out = ctx->status.as<int32_t>();
+    a.state_out = out->amps.p;
+    a.gate_count = ctx->counters.as<unsigned long long>() + 1;
+    a.c64 = c64;
+    QSB_CUDA(launch_resident(a, ctx->num_sms, ctx->stream));
+    float ms = timer.stop();
+    rc = check_sticky();
+    if (rc) return rc;
+    finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
+    return QSB_OK;
+  }
+  PlanDev* pd;
+  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+  if (rc) return rc;
+  StreamRun r{tp, pd, c64, 1, out->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
+  rc = run_stream(ctx, r);
+  if (rc) return rc;
+  float ms = timer.stop();
+  rc = check_sticky();
+  if (rc) return rc;
+  finish_stats(ctx, ms, pass_ms_sum(ctx, pd->plan.passes.size()), r.pass_bytes, r.passes, r.decides, r.launches, 1,
+               pd->plan.k);
+  return QSB_OK;
+}
+
+int32_t qsb_sample_static(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
+                          int64_t shot_count, uint64_t* bits_out) {
+  if (shot_count < 1) return fail(QSB_ERR_SIM, "shots must be >= 1");
+  const TapeInfo& t = tp->info;
+  if (t.needs_trajectories) return fail(QSB_ERR_ARG, "tape needs trajectories");
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  qsb_tape view = tp->gates_only ? tp->gates_only.get() : tp;
+  qsb_state st = nullptr;
+  int rc = qsb_state_create(ctx, t.n, precision, &st);
+  if (rc) return rc;
+  rc = qsb_statevector(view, params, st);
+  if (rc) {
+    qsb_state_destroy(st);
+    return rc;
+  }
+  std::vector<int32_t> mq, mb;
+  for (int idx : t.top_measures) {
+    mq.push_back(t.dev[idx].qubit);
+    mb.push_back(t.dev[idx].bit);
+  }
+  size_t N = (size_t)1 << t.n;
+  cudaError_t e = ctx->misc.ensure(sizeof(double) * N + 64);
+  if (e == cudaSuccess) e = ctx->misc2.ensure(sizeof(int32_t) * 2 * (mq.size() + 1) + sizeof(uint64_t) * t.nwords * shot_count);
+  if (e != cudaSuccess) {
+    qsb_state_destroy(st);
+    return fail(QSB_ERR_OOM, cudaGetErrorString(e));
+  }
+  int32_t* d_mq = ctx->misc2.as<int32_t>();
+  int32_t* d_mb = d_mq + mq.size() + 1;
+  uint64_t* d_bits = reinterpret_cast<uint64_t*>(ctx->misc2.as<char>() + sizeof(int32_t) * 2 * (mq.size() + 1));
+  d_bits = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(d_bits) + 7) & ~uintptr_t(7));
+  if (!mq.empty()) {
+    QSB_CUDA(cudaMemcpyAsync(d_mq, mq.data(), sizeof(int32_t) * mq.size(), cudaMemcpyHostToDevice, ctx->stream));
+    QSB_CUDA(cudaMemcpyAsync(d_mb, mb.data(), sizeof(int32_t) * mb.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  launch_cumsum_seq(st->c64, st->amps.p, t.n, ctx->misc.as<double>(), ctx->stream);
+  launch_static_search(ctx->misc.as<double>(), t.n, seed, shot_begin, shot_count, d_mq, d_mb, (int)mq.size(), t.nwords,
+                       d_bits, ctx->stream);
+  e = cudaMemcpyAsync(bits_out, d_bits, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  qsb_state_destroy(st);
+  if (e != cudaSuccess) return fail(QSB_ERR_CUDA, cudaGetErrorString(e));
+  return check_sticky();
+}
+
+int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_t npoints, const uint64_t* xmask,
+                    const uint64_t* zmask, const int32_t* ny, const double* coef, int32_t nterms, double* energies_out,
+                    double* term_out) {
+  const TapeInfo& t = tp->info;
+  if (t.top_level_dynamic) return fail(QSB_ERR_DYNAMIC, "observe needs a static kernel");
+  if (npoints < 1) return fail(QSB_ERR_ARG, "npoints must be >= 1");
+  uint64_t qm = t.n >= 64 ? ~0ull : ((1ull << t.n) - 1);
+  for (int i = 0; i < nterms; ++i)
+    if ((xmask[i] & ~qm) || (zmask[i] & ~qm)) return fail(QSB_ERR_BAD_PAULI, "pauli mask outside the register");
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  const int c64 = precision == QSB_C64 ? 1 : 0;
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  RunTimer timer(ctx);
+  PlanDev* pd;
+  int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+  if (rc) return rc;
+  int64_t B = pick_batch(ctx, t, pd->plan, c64, npoints);
+  QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
+  std::vector<double> terms((size_t)std::max(1, nterms) * B);
+  double pass_ms = 0, pass_bytes = 0;
+  int64_t passes = 0, decides = 0, launches = 0;
+  for (int64_t off = 0; off < npoints; off += B) {
+    int64_t b = std::min(B, npoints - off);
+    const double* d_params = nullptr;
+    rc = upload_params(tp, t.nparams ? params + off * t.nparams : nullptr, b, &d_params);
+    if (rc) return rc;
+    const double* mats;
+    int64_t mstride;
+    if (t.has_param_angles && !t.mats.empty()) {
+      size_t per = t.mats.size() * 8;
+      QSB_CUDA(ctx->mats.ensure(per * sizeof(double) * b));
+      launch_mats_prep(tp->d_matsrc.as<MatSrc>(), (int)t.mats.size(), d_params, t.nparams, b, ctx->mats.as<double>(),
+                       ctx->stream);
+      mats = ctx->mats.as<double>();
+      mstride = (int64_t)per;
+    } else {
+      mats = tp->d_mats.as<double>();
+      mstride = 0;
+    }
+    StreamRun r{tp, pd, c64, b, ctx->state.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
+    rc = run_stream(ctx, r);
+    if (rc) return rc;
+    pass_bytes += r.pass_bytes;
+    passes += r.passes;
+    decides += r.decides;
+    launches += r.launches;
+    if (nterms > 0) {
+      rc = expval_terms(ctx, c64, ctx->state.p, t.n, b, xmask, zmask, ny, nterms, terms.data());
+      if (rc) return rc;
+    }
+    pass_ms += pass_ms_sum(ctx, pd->plan.passes.size());
+    for (int64_t p = 0; p < b; ++p) {
+      double e = 0.0;
+      for (int i = 0; i < nterms; ++i) e += coef[i] * terms[p * nterms + i];
+      energies_out[off + p] = e;
+      if (term_out)
+        for (int i = 0; i < nterms; ++i) term_out[(off + p) * nterms + i] = terms[p * nterms + i];
+    }
+  }
+  float ms = timer.stop();
+  rc = check_sticky();
+  if (rc) return rc;
+  finish_stats(ctx, ms, pass_ms, pass_bytes, passes, decides, launches, 1, pd->plan.k);
+  return QSB_OK;
+}
+
+}  // extern "C"
+
+namespace qsb {
+void launch_debug_rng(uint64_t seed, int64_t shot, int count, double* out, cudaStream_t s);
+}
+
+extern "C" int32_t qsb_debug_rng(qsb_ctx ctx, uint64_t seed, int64_t shot, int32_t count, double* out) {
+  if (count < 0) return fail(QSB_ERR_ARG, "negative count");
+  DeviceGuard g(ctx->device);
+  QSB_CUDA(ctx->misc.ensure(sizeof(double) * (count + 1)));
+  qsb::launch_debug_rng(seed, shot, count, ctx->misc.as<double>(), ctx->stream);
+  QSB_CUDA(cudaMemcpyAsync(out, ctx->misc.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}

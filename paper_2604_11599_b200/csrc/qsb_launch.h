@@ -1,0 +1,112 @@
+// Host-callable launchers for the sm_100a kernels (precision-dispatched).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "qsb_internal.h"
+
+namespace qsb {
+
+constexpr int kResMaxWords = 16;  // classical words kept in shared memory by the resident engine
+
+// ---- single-state kernels (qsb_state.cu) -----------------------------------
+void launch_init_zero(int c64, void* amps, int n, int64_t slots, cudaStream_t s);
+void launch_apply_1q(int c64, void* amps, int n, int t, uint64_t cm, uint64_t cv, int gclass,
+                     const double* m8, cudaStream_t s);
+void launch_apply_swap(int c64, void* amps, int n, int t0, int t1, uint64_t cm, uint64_t cv, cudaStream_t s);
+// deterministic sum of |a|^2 over indices with bit q == 1 (q < 0: all indices) -> *out_dev
+void launch_prob(int c64, const void* amps, int n, int q, double* scratch, double* out_dev, cudaStream_t s);
+int prob_scratch_len(int n);
+void launch_collapse(int c64, void* amps, int n, int q, int outcome, double scale, int flip, cudaStream_t s);
+void launch_c128_to_c64(const double* in, float* out, int64_t count, cudaStream_t s);
+void launch_c64_to_c128(const float* in, double* out, int64_t count, cudaStream_t s);
+
+// Pauli expectation over `slots` states: one launch per X-mask group of <= 8 terms.
+struct PauliGroup {
+  uint64_t xmask;
+  int32_t nterm;
+  int32_t term0;          // first output term index
+  uint64_t zy[8];         // Z|Y masks
+  int32_t ny[8];
+};
+int expval_blocks(int n);
+void launch_expval_group(int c64, const void* amps, int n, int64_t slots, const PauliGroup& g,
+                         double* partial /*[slots][nterm_total][blocks]*/, int nterm_total, cudaStream_t s);
+void launch_expval_finish(const double* partial, int64_t slots, int nterm_total, int blocks,
+                          const uint64_t* xmask, const int32_t* ny, double* out /*[slots][nterm]*/, cudaStream_t s);
+
+// static sampling
+void launch_cumsum_seq(int c64, const void* amps, int n, double* cdf, cudaStream_t s);
+void launch_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
+                          const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits,
+                          cudaStream_t s);
+
+// ---- resident engine (qsb_resident.cu) -------------------------------------
+struct ResidentArgs {
+  const DevOp* ops;
+  int32_t nops;
+  int32_t n;
+  int32_t nwords;
+  int32_t predrawn_stride;
+  const double* mats;
+  int64_t mat_stride;     // doubles between slots' matrix tables (0 = shared)
+  uint64_t seed;
+  int64_t shot_begin;
+  int64_t count;
+  const double* predrawn; // [count][predrawn_stride] or null
+  uint64_t* bits_out;     // [count][nwords]
+  int32_t* status_out;    // [count]
+  void* state_out;        // final state of slot 0 (or null)
+  int64_t* trace_out;     // slot 0 trace (or null)
+  int32_t max_trace;
+  int32_t* ntrace_out;
+  unsigned long long* tie_count;
+  unsigned long long* gate_count;
+  const uint64_t* rng_init;  // slot 0 starts from these words (or null: for_shot)
+  uint64_t* rng_final;       // slot 0 RNG words after the run (or null)
+  int32_t* draws_out;        // slot 0 uniforms consumed (or null)
+  int32_t c64;
+};
+int resident_max_qubits(int c64);
+cudaError_t launch_resident(const ResidentArgs& a, int num_sms, cudaStream_t s);
+
+// ---- streaming engine (qsb_stream.cu) --------------------------------------
+void launch_mats_prep(const MatSrc* src, int nmat, const double* params, int nparams, int64_t slots,
+                      double* mats_out, cudaStream_t s);
+void launch_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards, int gwords, int64_t slots,
+                     uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, cudaStream_t s);
+
+struct StreamArgs {
+  void* state;
+  int32_t n;
+  int32_t c64;
+  const PassGate* gates;
+  const double* mats;
+  int64_t mat_stride;
+  TrajCtl* ctl;
+  uint64_t* bits;
+  int32_t nwords;
+  int32_t gwords;
+  uint32_t* guards;
+  double* partial;
+  int64_t partial_stride;   // doubles per slot
+  int64_t slots;
+  // decide
+  const DevOp* region_ops;
+  const double* predrawn;
+  int32_t predrawn_stride;
+  int32_t ntiles_log2;
+  int64_t predrawn_slot0;   // global slot index of slot 0 (row of predrawn)
+  unsigned long long* tie_count;
+  int64_t* trace_out;
+  int32_t max_trace;
+  int32_t* ntrace_out;
+};
+cudaError_t launch_pass(const StreamArgs& a, const PassDesc& pd, cudaStream_t s);
+cudaError_t launch_decide(const StreamArgs& a, const RegionDesc& rd, cudaStream_t s);
+void launch_count_gates(const StreamArgs& a, const int32_t* guard_gates, int nguards, int64_t unguarded,
+                        unsigned long long* out, cudaStream_t s);
+// out[i] = collapse(state[i ^ frame]) for slot 0; `clear` = frame bits already cleared by
+// passes after the last decide, `consumed` = a pass already applied the pending collapse
+void launch_finalize(const StreamArgs& a, void* out, uint64_t clear, int consumed, cudaStream_t s);
+
+}  // namespace qsb

@@ -1,0 +1,449 @@
+// Tape analysis (Kernel IR -> flattened device program) and the fused-pass planner.
+//
+// Reference semantics preserved here:
+//   * _needs_trajectories (sim.py:322-335): top-level scan only.
+//   * _scan_static (sim.py:394-399): statevector refuses any top-level Measure /
+//     CondBlock / Reset.
+//   * CondBlock evaluates its predicate once at entry (sim.py:297): IF ops define a
+//     then-guard and an else-guard bit per trajectory, evaluated once.
+//
+// Streaming plan (state in HBM):
+//   gate region   -> greedy fused passes over k-qubit tiles (targets must be in the
+//                    tile; controls and diagonal targets may live outside it)
+//   measure region-> one "decide" step per trajectory that resolves every measure,
+//                    reset, predicate and collapsed-qubit Pauli/phase gate of the
+//                    region from the marginal of the measured qubits, computed by
+//                    the epilogue of the preceding pass; the collapse itself is
+//                    applied by the prologue of the next pass.
+#include "qsb_plan.h"
+
+#include <algorithm>
+#include <map>
+#include <sstream>
+
+namespace qsb {
+
+static int popc(uint64_t v) { return __builtin_popcountll(v); }
+
+static int gate_class_of(int base) {
+  switch (base) {
+    case QSB_G_X: return GC_XPERM;
+    case QSB_G_Y: return GC_ANTI;
+    case QSB_G_Z: case QSB_G_S: case QSB_G_T: case QSB_G_RZ: case QSB_G_P: return GC_DIAG;
+    case QSB_G_SWAP: return GC_SWAP;
+    default: return GC_DENSE;
+  }
+}
+
+std::string analyze_tape(const qsb_op* ops, int nops, int n, int nbits, int nparams, TapeInfo& out) {
+  std::ostringstream err;
+  if (n < 0 || n > kMaxQubits) {
+    err << "qubit count " << n << " outside [0, " << kMaxQubits << "]";
+    return err.str();
+  }
+  if (nbits < 0 || nparams < 0 || nops < 0) return "negative size";
+  out = TapeInfo();
+  out.n = n;
+  out.nbits = nbits;
+  out.nwords = std::max(1, (nbits + 63) / 64);
+  out.nparams = nparams;
+  const uint64_t qmask = n >= 64 ? ~0ull : ((1ull << n) - 1);
+  struct Open { int g_then, g_else; bool else_seen; };
+  std::vector<Open> stack;
+  std::vector<int> path;
+  int g = 0;
+  uint64_t measured_top = 0;
+  for (int i = 0; i < nops; ++i) {
+    const qsb_op& o = ops[i];
+    DevOp d{};
+    d.kind = o.kind;
+    d.op_index = i;
+    d.guard = path.empty() ? -1 : path.back();
+    d.mat = -1;
+    d.mj = -1;
+    const bool top = stack.empty();
+    switch (o.kind) {
+      case QSB_OP_GATE: {
+        if (o.base < 0 || o.base > QSB_G_SWAP) { err << "op " << i << ": bad gate base " << o.base; return err.str(); }
+        int nt = o.base == QSB_G_SWAP ? 2 : 1;
+        if (o.ntargets != nt) { err << "op " << i << ": gate takes " << nt << " target(s)"; return err.str(); }
+        uint64_t tm = 0;
+        for (int j = 0; j < nt; ++j) {
+          if (o.target[j] < 0 || o.target[j] >= n) { err << "op " << i << ": target out of range"; return err.str(); }
+          if (tm & (1ull << o.target[j])) { err << "op " << i << ": repeated target"; return err.str(); }
+          tm |= 1ull << o.target[j];
+        }
+        if ((o.ctrl_mask & ~qmask) || (o.ctrl_mask & tm) || (o.ctrl_val & ~o.ctrl_mask)) {
+          err << "op " << i << ": bad control mask";
+          return err.str();
+        }
+        d.gclass = gate_class_of(o.base);
+        d.t0 = o.target[0];
+        d.t1 = nt == 2 ? o.target[1] : -1;
+        d.cm = o.ctrl_mask;
+        d.cv = o.ctrl_val;
+        d.diag_one0 = (o.base == QSB_G_Z || o.base == QSB_G_S || o.base == QSB_G_T || o.base == QSB_G_P) ? 1 : 0;
+        MatSrc m{};
+        m.base = o.base;
+        m.adjoint = o.adjoint ? 1 : 0;
+        m.has_matrix = o.has_matrix ? 1 : 0;
+        for (int j = 0; j < 3; ++j) {
+          m.slot[j] = o.angle_slot[j];
+          m.angle[j] = o.angle[j];
+          if (o.angle_slot[j] >= 0) {
+            if (o.angle_slot[j] >= nparams) { err << "op " << i << ": parameter slot out of range"; return err.str(); }
+            m.has_matrix = 0;
+            out.has_param_angles = true;
+          }
+        }
+        for (int j = 0; j < 8; ++j) m.mat[j] = o.mat[j];
+        d.mat = (int)out.mats.size();
+        out.mats.push_back(m);
+        if (top && measured_top) out.needs_trajectories = true;
+      } break;
+      case QSB_OP_MEASURE:
+      case QSB_OP_RESET: {
+        if (o.qubit < 0 || o.qubit >= n) { err << "op " << i << ": qubit out of range"; return err.str(); }
+        d.qubit = o.qubit;
+        if (o.kind == QSB_OP_MEASURE) {
+          if (o.bit < 0 || o.bit >= nbits) { err << "op " << i << ": classical bit out of range"; return err.str(); }
+          d.bit = o.bit;
+        }
+        out.draws_max++;
+        if (top) {
+          out.top_level_dynamic = true;
+          if (o.kind == QSB_OP_RESET) out.needs_trajectories = true;
+          else {
+            if (measured_top & (1ull << o.qubit)) out.needs_trajectories = true;
+            measured_top |= 1ull << o.qubit;
+            out.top_measures.push_back((int)out.dev.size());
+          }
+        }
+      } break;
+      case QSB_OP_IF: {
+        if (o.pred_width < 1 || o.pred_width > 64 || o.pred_bit < 0 || o.pred_bit + o.pred_width > nbits ||
+            o.pred_cmp < 0 || o.pred_cmp > QSB_CMP_TRUTHY) {
+          err << "op " << i << ": bad predicate";
+          return err.str();
+        }
+        if (top) { out.needs_trajectories = true; out.top_level_dynamic = true; }
+        d.pred_cmp = o.pred_cmp;
+        d.pred_bit = o.pred_bit;
+        d.pred_width = o.pred_width;
+        d.pred_rhs = o.pred_rhs;
+        d.g_then = g++;
+        d.g_else = g++;
+        stack.push_back({d.g_then, d.g_else, false});
+        path.push_back(d.g_then);
+      } break;
+      case QSB_OP_ELSE: {
+        if (stack.empty() || stack.back().else_seen) { err << "op " << i << ": ELSE without IF"; return err.str(); }
+        stack.back().else_seen = true;
+        d.g_then = stack.back().g_then;
+        d.g_else = stack.back().g_else;
+        path.back() = d.g_else;
+        d.guard = path.size() >= 2 ? path[path.size() - 2] : -1;
+      } break;
+      case QSB_OP_ENDIF: {
+        if (stack.empty()) { err << "op " << i << ": ENDIF without IF"; return err.str(); }
+        d.g_then = stack.back().g_then;
+        d.g_else = stack.back().g_else;
+        stack.pop_back();
+        path.pop_back();
+        d.guard = path.empty() ? -1 : path.back();
+      } break;
+      default:
+        err << "op " << i << ": unknown kind " << o.kind;
+        return err.str();
+    }
+    out.dev.push_back(d);
+  }
+  if (!stack.empty()) return "unterminated IF";
+  out.nguards = g;
+  out.gwords = std::max(1, (g + 31) / 32);
+  return "";
+}
+
+// ---------------------------------------------------------------------------
+// streaming plan
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct RegionBuild {
+  RegionDesc desc{};
+  std::vector<DevOp> ops;
+  std::vector<int> mq;
+  std::map<int, std::vector<int>> collapsed_at;  // qubit -> guard path of its measure / reset
+};
+
+bool is_prefix(const std::vector<int>& a, const std::vector<int>& b) {
+  if (a.size() > b.size()) return false;
+  return std::equal(a.begin(), a.end(), b.begin());
+}
+
+struct Planner {
+  const TapeInfo& t;
+  int k, lowq;
+  StreamPlan& P;
+  std::vector<RegionBuild> regions;
+
+  Planner(const TapeInfo& t_, int k_, int lowq_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), P(p) {}
+
+  uint64_t low_mask() const { return lowq >= 64 ? ~0ull : ((1ull << lowq) - 1); }
+
+  void emit_pass(uint64_t S, const std::vector<int>& chosen, int epi_region) {
+    // fill S up to k qubits with the lowest unused qubits (longest contiguous runs)
+    for (int q = 0; q < t.n && popc(S) < k; ++q) S |= 1ull << q;
+    PassDesc pd{};
+    pd.smask = S;
+    pd.k = popc(S);
+    pd.lowq = lowq;
+    int pos[64];
+    int j = 0;
+    for (int q = 0; q < t.n; ++q) {
+      pos[q] = -1;
+      if (S >> q & 1) { pd.sq[j] = q; pos[q] = j++; }
+    }
+    pd.gate_begin = (int)P.gates.size();
+    for (int gi : chosen) {
+      const DevOp& d = t.dev[gi];
+      PassGate pg{};
+      pg.gclass = d.gclass;
+      pg.guard = d.guard;
+      pg.mat = d.mat;
+      pg.diag_one0 = d.diag_one0;
+      if (d.gclass == GC_DIAG && pos[d.t0] < 0) {
+        pg.gclass = GC_DIAG_GLOBAL;
+        pg.gq = d.t0;
+      } else {
+        pg.lt = pos[d.t0];
+        pg.lt2 = d.t1 >= 0 ? pos[d.t1] : -1;
+      }
+      for (uint64_t m = d.cm; m; m &= m - 1) {
+        int q = __builtin_ctzll(m);
+        uint64_t v = (d.cv >> q) & 1;
+        if (pos[q] >= 0) {
+          pg.lcm |= 1u << pos[q];
+          pg.lcv |= (uint32_t)v << pos[q];
+        } else {
+          pg.gcm |= 1ull << q;
+          pg.gcv |= v << q;
+        }
+      }
+      if (d.guard >= 0) P.guard_gates[d.guard]++;
+      else P.unguarded_gates++;
+      P.gates.push_back(pg);
+    }
+    pd.gate_count = (int)chosen.size();
+    pd.region = epi_region;
+    pd.epi = epi_region >= 0 ? 1 : 0;
+    P.passes.push_back(pd);
+    P.steps.push_back({0, (int)P.passes.size() - 1});
+  }
+
+  // greedy first-fit fusion of one gate region
+  void flush(std::vector<int>& buf, int epi_region) {
+    if (buf.empty()) {
+      if (epi_region >= 0) emit_pass(low_mask(), {}, epi_region);
+      return;
+    }
+    std::vector<int> remaining = buf;
+    while (!remaining.empty()) {
+      uint64_t S = low_mask();
+      uint64_t blocked = 0;
+      std::vector<int> chosen, rest;
+      for (int gi : remaining) {
+        const DevOp& d = t.dev[gi];
+        uint64_t tm = (1ull << d.t0) | (d.t1 >= 0 ? (1ull << d.t1) : 0);
+        uint64_t touched = tm | d.cm;
+        if (touched & blocked) {
+          rest.push_back(gi);
+          blocked |= touched;
+          continue;
+        }
+        uint64_t need = d.gclass == GC_DIAG ? 0 : (tm & ~S);
+        if (popc(S | need) <= k) {
+          S |= need;
+          chosen.push_back(gi);
+        } else {
+          rest.push_back(gi);
+          blocked |= touched;
+        }
+      }
+      bool last = rest.empty();
+      emit_pass(S, chosen, last ? epi_region : -1);
+      remaining.swap(rest);
+    }
+    buf.clear();
+  }
+
+  bool descriptor_ok(const DevOp& d, const RegionBuild& R, const std::vector<int>& path) const {
+    if (d.gclass != GC_XPERM && d.gclass != GC_ANTI && d.gclass != GC_DIAG) return false;
+    uint64_t qs = (1ull << d.t0) | d.cm;
+    for (uint64_t m = qs; m; m &= m - 1) {
+      int q = __builtin_ctzll(m);
+      auto it = R.collapsed_at.find(q);
+      if (it == R.collapsed_at.end() || !is_prefix(it->second, path)) return false;
+    }
+    return true;
+  }
+
+  std::string run() {
+    P.guard_gates.assign(std::max(1, t.nguards), 0);
+    regions.emplace_back();  // R0: guards evaluated before the first measurement
+    P.steps.push_back({1, 0});
+    int cur = 0;
+    bool meas_mode = false;
+    std::vector<int> buf;
+    std::vector<int> path;
+    for (int i = 0; i < (int)t.dev.size(); ++i) {
+      const DevOp& d = t.dev[i];
+      switch (d.kind) {
+        case QSB_OP_IF:
+          regions[cur].ops.push_back(d);
+          path.push_back(d.g_then);
+          break;
+        case QSB_OP_ELSE:
+          regions[cur].ops.push_back(d);
+          path.back() = d.g_else;
+          break;
+        case QSB_OP_ENDIF:
+          regions[cur].ops.push_back(d);
+          path.pop_back();
+          break;
+        case QSB_OP_MEASURE:
+        case QSB_OP_RESET: {
+          bool fresh = !meas_mode;
+          if (meas_mode) {
+            auto& mq = regions[cur].mq;
+            bool known = std::find(mq.begin(), mq.end(), d.qubit) != mq.end();
+            if (!known && (int)mq.size() == kMaxMeasureRegion) fresh = true;
+          }
+          if (fresh) {
+            regions.emplace_back();
+            int r = (int)regions.size() - 1;
+            regions[r].desc.has_marginal = 1;
+            flush(buf, r);
+            P.steps.push_back({1, r});
+            cur = r;
+            meas_mode = true;
+          }
+          RegionBuild& R = regions[cur];
+          if (std::find(R.mq.begin(), R.mq.end(), d.qubit) == R.mq.end()) R.mq.push_back(d.qubit);
+          R.collapsed_at[d.qubit] = path;
+          R.ops.push_back(d);
+        } break;
+        case QSB_OP_GATE:
+          if (meas_mode && descriptor_ok(d, regions[cur], path)) {
+            regions[cur].ops.push_back(d);
+            regions[cur].desc.desc_gates++;
+            break;
+          }
+          meas_mode = false;
+          buf.push_back(i);
+          break;
+      }
+    }
+    flush(buf, -1);
+    return finish();
+  }
+
+  std::string finish() {
+    // regions: M ordering, M-index views of ops, epilogue bin maps
+    for (int r = 0; r < (int)regions.size(); ++r) {
+      RegionBuild& R = regions[r];
+      RegionDesc& rd = R.desc;
+      rd.mcount = (int)R.mq.size();
+      rd.mmask = 0;
+      for (int j = 0; j < rd.mcount; ++j) {
+        rd.mq[j] = R.mq[j];
+        rd.mmask |= 1ull << R.mq[j];
+      }
+      auto midx = [&](int q) {
+        for (int j = 0; j < rd.mcount; ++j)
+          if (rd.mq[j] == q) return j;
+        return -1;
+      };
+      rd.op_begin = (int)P.region_ops.size();
+      for (DevOp d : R.ops) {
+        if (d.kind == QSB_OP_MEASURE || d.kind == QSB_OP_RESET) d.mj = midx(d.qubit);
+        if (d.kind == QSB_OP_GATE) {
+          d.mj = midx(d.t0);
+          d.mcm = d.mcv = 0;
+          for (uint64_t m = d.cm; m; m &= m - 1) {
+            int q = __builtin_ctzll(m);
+            int j = midx(q);
+            if (j < 0) return "internal: descriptor control outside M";
+            d.mcm |= 1ull << j;
+            d.mcv |= ((d.cv >> q) & 1ull) << j;
+          }
+        }
+        P.region_ops.push_back(d);
+      }
+      rd.op_end = (int)P.region_ops.size();
+      for (int j = 0; j < kMaxMeasureRegion; ++j) rd.mloc_bit[j] = rd.mtile_bit[j] = -1;
+    }
+    // link epilogue passes to their regions
+    for (PassDesc& pd : P.passes) {
+      if (!pd.epi) continue;
+      RegionDesc& rd = regions[pd.region].desc;
+      rd.epi_smask = pd.smask;
+      pd.mmask = rd.mmask;
+      int ml = 0;
+      for (int j = 0; j < rd.mcount; ++j) {
+        int q = rd.mq[j];
+        if (pd.smask >> q & 1) {
+          int lp = popc(pd.smask & ((1ull << q) - 1));
+          pd.mloc[ml] = lp;
+          rd.mloc_bit[j] = ml++;
+        } else {
+          uint64_t nons = ~pd.smask & ((1ull << q) - 1);
+          rd.mtile_bit[j] = popc(nons & (t.n >= 64 ? ~0ull : ((1ull << t.n) - 1)));
+        }
+      }
+      pd.m_local = ml;
+      rd.m_local = ml;
+      P.max_local_bins = std::max(P.max_local_bins, 1 << ml);
+    }
+    // prologue / init / frame-clear bookkeeping in step order
+    uint64_t acc = 0;
+    bool pending = false, first_pass = true;
+    for (const Step& s : P.steps) {
+      if (s.type == 0) {
+        PassDesc& pd = P.passes[s.index];
+        pd.clear_before = acc;
+        acc |= pd.smask;
+        pd.prologue = pending ? 1 : 0;
+        pending = false;
+        pd.init_zero = first_pass ? 1 : 0;
+        first_pass = false;
+      } else {
+        RegionDesc& rd = regions[s.index].desc;
+        rd.clear_mask = acc;
+        acc = 0;
+        if (rd.has_marginal) pending = true;
+      }
+    }
+    for (auto& R : regions) {
+      P.regions.push_back(R.desc);
+      P.descriptor_gates += R.desc.desc_gates;
+    }
+    return "";
+  }
+};
+
+}  // namespace
+
+std::string build_stream_plan(const TapeInfo& t, int k, int lowq, StreamPlan& out) {
+  out = StreamPlan();
+  k = std::max(1, std::min(k, std::min(t.n, kMaxTile)));
+  lowq = std::max(0, std::min(lowq, k));
+  out.k = k;
+  out.lowq = lowq;
+  out.ntiles_log2 = t.n - k;
+  Planner pl(t, k, lowq, out);
+  return pl.run();
+}
+
+}  // namespace qsb

@@ -1,0 +1,45 @@
+// Host-side tape analysis and the fused-pass planner.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "qsb_internal.h"
+
+namespace qsb {
+
+struct TapeInfo {
+  int n = 0, nbits = 0, nwords = 1, nparams = 0, nguards = 0, gwords = 1;
+  bool needs_trajectories = false;  // sim.py:322-335
+  bool top_level_dynamic = false;   // sim.py:394-399 (statevector refuses)
+  bool has_param_angles = false;
+  int draws_max = 0;                // upper bound on uniforms consumed by one shot
+  std::vector<DevOp> dev;           // flattened program (all ops, program order)
+  std::vector<MatSrc> mats;         // one per GATE op (DevOp.mat)
+  std::vector<int> top_measures;    // dev indices of top-level MEASURE ops (static sampling)
+};
+
+// Validates caller ops and builds the flattened device program.  Returns an error
+// message (empty on success).
+std::string analyze_tape(const qsb_op* ops, int nops, int n, int nbits, int nparams, TapeInfo& out);
+
+struct Step {
+  int type;   // 0 = pass, 1 = decide
+  int index;
+};
+
+struct StreamPlan {
+  int k = 0, lowq = 0, ntiles_log2 = 0;
+  std::vector<PassDesc> passes;
+  std::vector<PassGate> gates;
+  std::vector<RegionDesc> regions;
+  std::vector<DevOp> region_ops;
+  std::vector<Step> steps;
+  int max_local_bins = 1;           // max 2^|M∩S| over epilogue passes
+  std::vector<int32_t> guard_gates; // pass gates guarded directly by each guard id
+  int64_t unguarded_gates = 0;
+  int64_t descriptor_gates = 0;     // gates folded into decide regions
+};
+
+std::string build_stream_plan(const TapeInfo& t, int k, int lowq, StreamPlan& out);
+
+}  // namespace qsb

@@ -1,0 +1,324 @@
+// Single-state kernels: the per-op surface of sim.py (apply_gate, measure, reset,
+// norm, expval_pauli) plus static sampling.  One state vector of 2^n interleaved
+// complex amplitudes (or `slots` of them back to back).
+//
+// All reductions are deterministic: fixed grid as a function of n only, fixed-order
+// warp trees (shfl_down, lane 0 result) and a fixed-order final sum -- no float
+// atomics anywhere, so repeated runs are bit-identical.
+#include <cuda_runtime.h>
+
+#include "qsb_device.cuh"
+#include "qsb_launch.h"
+
+namespace qsb {
+
+namespace {
+
+constexpr int kT = 256;
+
+template <int T> __device__ double block_sum(double v, double* sh) {
+  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < T / 32; ++w) tot += sh[w];
+  return tot;  // valid in thread 0
+}
+
+template <typename R> __global__ void k_init_zero(typename Amp<R>::T* amps, int n, int64_t total) {
+  int64_t N = 1ll << n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    amps[i] = mk<R>((i % N) == 0 ? (R)1 : (R)0, (R)0);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kT) k_apply_1q(typename Amp<R>::T* amps, int n, int t, uint64_t cm, uint64_t cv,
+                                                 int gc, double m0, double m1, double m2, double m3, double m4,
+                                                 double m5, double m6, double m7) {
+  const double m[8] = {m0, m1, m2, m3, m4, m5, m6, m7};
+  int64_t pairs = 1ll << (n - 1);
+  for (int64_t p = blockIdx.x * (int64_t)kT + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * kT) {
+    uint64_t i0 = insert_zero((uint64_t)p, t);
+    if ((i0 & cm) != cv) continue;
+    uint64_t i1 = i0 | (1ull << t);
+    auto a0 = amps[i0], a1 = amps[i1];
+    apply_pair<R>(gc, m, a0, a1);
+    amps[i0] = a0;
+    amps[i1] = a1;
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kT) k_apply_swap(typename Amp<R>::T* amps, int n, int t0, int t1, uint64_t cm,
+                                                   uint64_t cv) {
+  int lo = t0 < t1 ? t0 : t1, hi = t0 < t1 ? t1 : t0;
+  int64_t quads = 1ll << (n - 2);
+  for (int64_t p = blockIdx.x * (int64_t)kT + threadIdx.x; p < quads; p += (int64_t)gridDim.x * kT) {
+    uint64_t base = insert_zero(insert_zero((uint64_t)p, lo), hi);
+    if ((base & cm) != cv) continue;
+    uint64_t a = base | (1ull << t0), b = base | (1ull << t1);
+    auto x = amps[a];
+    amps[a] = amps[b];
+    amps[b] = x;
+  }
+}
+
+int prob_blocks(int n) {
+  int64_t items = n >= 1 ? (1ll << (n - 1)) : 1;
+  int64_t b = (items + kT * 8 - 1) / (kT * 8);
+  if (b > 2048) b = 2048;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kT) k_prob_partial(const typename Amp<R>::T* amps, int n, int q, double* part) {
+  __shared__ double sh[kT / 32];
+  double acc = 0.0;
+  if (q >= 0) {
+    int64_t items = 1ll << (n - 1);
+    for (int64_t p = blockIdx.x * (int64_t)kT + threadIdx.x; p < items; p += (int64_t)gridDim.x * kT)
+      acc += norm2<R>(amps[insert_zero((uint64_t)p, q) | (1ull << q)]);
+  } else {
+    int64_t items = 1ll << n;
+    for (int64_t p = blockIdx.x * (int64_t)kT + threadIdx.x; p < items; p += (int64_t)gridDim.x * kT)
+      acc += norm2<R>(amps[p]);
+  }
+  double tot = block_sum<kT>(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void k_sum_seq(const double* part, int cnt, double* out) {
+  double s = 0.0;
+  for (int i = 0; i < cnt; ++i) s += part[i];
+  *out = s;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kT) k_collapse(typename Amp<R>::T* amps, int n, int q, int outcome, double scale,
+                                                 int flip) {
+  int64_t pairs = 1ll << (n - 1);
+  R s = (R)scale;
+  for (int64_t p = blockIdx.x * (int64_t)kT + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * kT) {
+    uint64_t i0 = insert_zero((uint64_t)p, q), i1 = i0 | (1ull << q);
+    auto z = mk<R>(0, 0);
+    if (outcome) {
+      auto a1 = amps[i1];
+      a1 = mk<R>(a1.x * s, a1.y * s);
+      if (flip) {  // reset: x after the projection (sim.py:257-258)
+        amps[i0] = a1;
+        amps[i1] = z;
+      } else {
+        amps[i0] = z;
+        amps[i1] = a1;
+      }
+    } else {
+      auto a0 = amps[i0];
+      amps[i0] = mk<R>(a0.x * s, a0.y * s);
+      amps[i1] = z;
+    }
+  }
+}
+
+__global__ void k_c128_to_c64(const double* in, float* out, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+__global__ void k_c64_to_c128(const float* in, double* out, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
+// ---- Pauli expectation --------------------------------------------------------
+// <P> = sgn * sum over pairs (i, i^x), bit h(x) of i clear, of 2 s(i) * (ny odd ? Im c : Re c),
+// c = conj(psi_i) psi_{i^x}, s(i) = (-1)^popcount(i & zy), sgn = + for ny%4 in {0,1}
+// (SURVEY.md App. B identity); x = 0: sum_i s(i) |psi_i|^2.
+template <typename R>
+__global__ void __launch_bounds__(kT) k_expval(const typename Amp<R>::T* amps, int n, PauliGroup g, double* partial,
+                                               int nterm_total) {
+  __shared__ double sh[kT / 32];
+  const int64_t N = 1ll << n;
+  const typename Amp<R>::T* a = amps + (int64_t)blockIdx.y * N;
+  double acc[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t] = 0.0;
+  if (g.xmask == 0) {
+    for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < N; i += (int64_t)gridDim.x * kT) {
+      double w = norm2<R>(a[i]);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t < g.nterm) acc[t] += (__popcll((uint64_t)i & g.zy[t]) & 1) ? -w : w;
+    }
+  } else {
+    int h = 63 - __clzll(g.xmask);
+    int64_t pairs = N >> 1;
+    for (int64_t p = blockIdx.x * (int64_t)kT + threadIdx.x; p < pairs; p += (int64_t)gridDim.x * kT) {
+      uint64_t i = insert_zero((uint64_t)p, h);
+      auto u = a[i], v = a[i ^ g.xmask];
+      double ur = u.x, ui = u.y, vr = v.x, vi = v.y;
+      double cre = fma(ur, vr, ui * vi);
+      double cim = fma(ur, vi, -ui * vr);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (t < g.nterm) {
+          double val = (g.ny[t] & 1) ? cim : cre;
+          acc[t] += (__popcll(i & g.zy[t]) & 1) ? -val : val;
+        }
+      }
+    }
+  }
+  for (int t = 0; t < g.nterm; ++t) {
+    double tot = block_sum<kT>(acc[t], sh);
+    if (threadIdx.x == 0)
+      partial[((int64_t)blockIdx.y * nterm_total + g.term0 + t) * gridDim.x + blockIdx.x] = tot;
+  }
+}
+
+__global__ void k_expval_finish(const double* partial, int64_t slots, int nterm, int blocks, const uint64_t* xmask,
+                                const int32_t* ny, double* out) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= slots * nterm) return;
+  int t = (int)(idx % nterm);
+  const double* p = partial + idx * blocks;
+  double s = 0.0;
+  for (int b = 0; b < blocks; ++b) s += p[b];
+  if (xmask[t] != 0) s *= 2.0;
+  int r = ny[t] & 3;
+  out[idx] = (r >= 2) ? -s : s;
+}
+
+// ---- static sampling (sim.py:354-369) ---------------------------------------------
+template <typename R> __global__ void k_cumsum_seq(const typename Amp<R>::T* amps, int64_t N, double* cdf) {
+  // numpy.cumsum is a strict left-to-right sum; reproduce it exactly with one thread.
+  double c = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    c = __dadd_rn(c, norm2<R>(amps[i]));
+    cdf[i] = c;
+  }
+}
+
+__global__ void k_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
+                                const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  uint64_t rs[4];
+  rng_for_shot(rs, seed, (uint64_t)(shot_begin + s));
+  double u = rng_uniform(rs);
+  int64_t N = 1ll << n, lo = 0, hi = N;
+  while (lo < hi) {  // searchsorted(side="right"): first index with cdf > u
+    int64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] <= u) lo = mid + 1;
+    else hi = mid;
+  }
+  int64_t idx = lo < N - 1 ? lo : N - 1;
+  uint64_t* b = bits + s * nwords;
+  for (int w = 0; w < nwords; ++w) b[w] = 0;
+  for (int j = 0; j < nmeas; ++j) {  // later writes to the same bit win
+    int f = mb[j];
+    uint64_t v = ((uint64_t)idx >> mq[j]) & 1ull;
+    b[f >> 6] = (b[f >> 6] & ~(1ull << (f & 63))) | (v << (f & 63));
+  }
+}
+
+int grid_for(int64_t items) {
+  int64_t g = (items + kT - 1) / kT;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+void launch_init_zero(int c64, void* amps, int n, int64_t slots, cudaStream_t s) {
+  int64_t total = slots << n;
+  if (c64) k_init_zero<float><<<grid_for(total), kT, 0, s>>>((float2*)amps, n, total);
+  else k_init_zero<double><<<grid_for(total), kT, 0, s>>>((double2*)amps, n, total);
+}
+
+void launch_apply_1q(int c64, void* amps, int n, int t, uint64_t cm, uint64_t cv, int gclass, const double* m,
+                     cudaStream_t s) {
+  int g = grid_for(1ll << (n - 1));
+  if (c64)
+    k_apply_1q<float><<<g, kT, 0, s>>>((float2*)amps, n, t, cm, cv, gclass, m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7]);
+  else
+    k_apply_1q<double><<<g, kT, 0, s>>>((double2*)amps, n, t, cm, cv, gclass, m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7]);
+}
+
+void launch_apply_swap(int c64, void* amps, int n, int t0, int t1, uint64_t cm, uint64_t cv, cudaStream_t s) {
+  int g = grid_for(1ll << (n - 2));
+  if (c64) k_apply_swap<float><<<g, kT, 0, s>>>((float2*)amps, n, t0, t1, cm, cv);
+  else k_apply_swap<double><<<g, kT, 0, s>>>((double2*)amps, n, t0, t1, cm, cv);
+}
+
+int prob_scratch_len(int n) { return prob_blocks(n + 1); }
+
+void launch_prob(int c64, const void* amps, int n, int q, double* scratch, double* out, cudaStream_t s) {
+  int b = q >= 0 ? prob_blocks(n) : prob_blocks(n + 1);
+  if (c64) k_prob_partial<float><<<b, kT, 0, s>>>((const float2*)amps, n, q, scratch);
+  else k_prob_partial<double><<<b, kT, 0, s>>>((const double2*)amps, n, q, scratch);
+  k_sum_seq<<<1, 1, 0, s>>>(scratch, b, out);
+}
+
+void launch_collapse(int c64, void* amps, int n, int q, int outcome, double scale, int flip, cudaStream_t s) {
+  int g = grid_for(1ll << (n - 1));
+  if (c64) k_collapse<float><<<g, kT, 0, s>>>((float2*)amps, n, q, outcome, scale, flip);
+  else k_collapse<double><<<g, kT, 0, s>>>((double2*)amps, n, q, outcome, scale, flip);
+}
+
+void launch_c128_to_c64(const double* in, float* out, int64_t count, cudaStream_t s) {
+  k_c128_to_c64<<<grid_for(2 * count), kT, 0, s>>>(in, out, count);
+}
+void launch_c64_to_c128(const float* in, double* out, int64_t count, cudaStream_t s) {
+  k_c64_to_c128<<<grid_for(2 * count), kT, 0, s>>>(in, out, count);
+}
+
+int expval_blocks(int n) {
+  int64_t items = n >= 1 ? (1ll << (n - 1)) : 1;
+  int64_t b = (items + kT * 4 - 1) / (kT * 4);
+  if (b > 1024) b = 1024;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+void launch_expval_group(int c64, const void* amps, int n, int64_t slots, const PauliGroup& g, double* partial,
+                         int nterm_total, cudaStream_t s) {
+  dim3 grid(expval_blocks(n), (unsigned)slots);
+  if (c64) k_expval<float><<<grid, kT, 0, s>>>((const float2*)amps, n, g, partial, nterm_total);
+  else k_expval<double><<<grid, kT, 0, s>>>((const double2*)amps, n, g, partial, nterm_total);
+}
+
+void launch_expval_finish(const double* partial, int64_t slots, int nterm, int blocks, const uint64_t* xmask,
+                          const int32_t* ny, double* out, cudaStream_t s) {
+  int64_t items = slots * nterm;
+  k_expval_finish<<<(unsigned)((items + 127) / 128), 128, 0, s>>>(partial, slots, nterm, blocks, xmask, ny, out);
+}
+
+void launch_cumsum_seq(int c64, const void* amps, int n, double* cdf, cudaStream_t s) {
+  if (c64) k_cumsum_seq<float><<<1, 1, 0, s>>>((const float2*)amps, 1ll << n, cdf);
+  else k_cumsum_seq<double><<<1, 1, 0, s>>>((const double2*)amps, 1ll << n, cdf);
+}
+
+void launch_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
+                          const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits,
+                          cudaStream_t s) {
+  k_static_search<<<(unsigned)((count + 127) / 128), 128, 0, s>>>(cdf, n, seed, shot_begin, count, mq, mb, nmeas,
+                                                                 nwords, bits);
+}
+
+}  // namespace qsb
+
+namespace qsb {
+namespace {
+__global__ void k_debug_rng(uint64_t seed, int64_t shot, int count, double* out) {
+  uint64_t rs[4];
+  rng_for_shot(rs, seed, (uint64_t)shot);
+  for (int i = 0; i < count; ++i) out[i] = rng_uniform(rs);
+}
+}  // namespace
+void launch_debug_rng(uint64_t seed, int64_t shot, int count, double* out, cudaStream_t s) {
+  k_debug_rng<<<1, 1, 0, s>>>(seed, shot, count, out);
+}
+}  // namespace qsb

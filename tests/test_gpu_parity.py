@@ -1,0 +1,296 @@
+"""GPU parity: the B200 backend through the C ABI vs the reference (golden
+fixtures recorded from /root/reference by tests/golden/make_goldens.py) and vs
+the CPU oracle (oracle/sim_port.py, itself pinned bit-exact to the reference).
+
+Tolerances (north_star / SURVEY.md §4):
+  amplitudes, expectation values : 1e-10 (complex128), 1e-5 (complex64)
+  histograms, per-shot keys, branch traces, RNG words : bit-exact (complex128)
+"""
+
+import contextlib
+import math
+
+import numpy as np
+import pytest
+
+from oracle import sim_port as P
+from paper_2604_11599_b200 import _lib, ir, sim, workloads
+from paper_2604_11599_b200.errors import BadPauliString, DegenerateNorm, DynamicCircuit, SimError
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-10, "c64": 1e-5}
+
+
+def cvec(d):
+    return np.array(d["re"]) + 1j * np.array(d["im"])
+
+
+@contextlib.contextmanager
+def engine(which):
+    """which: 'auto' | 'resident' | 'stream'"""
+    ctx = _lib.context()
+    ctx.set_option("engine", {"auto": -1, "resident": 0, "stream": 1}[which])
+    try:
+        yield
+    finally:
+        ctx.set_option("engine", -1)
+
+
+@contextlib.contextmanager
+def option(key, value, reset):
+    ctx = _lib.context()
+    ctx.set_option(key, value)
+    try:
+        yield
+    finally:
+        ctx.set_option(key, reset)
+
+
+def assert_state(got, want, tol):
+    err = np.max(np.abs(np.asarray(got) - np.asarray(want))) if len(want) else 0.0
+    assert err <= tol, f"max |err| {err:.3e} > {tol}"
+
+
+# ---------------------------------------------------------------------------
+
+
+def test_device_rng_known_answers(golden):
+    ctx = _lib.context()
+    for case in golden("rng.json")["for_shot"]:
+        out = np.zeros(6)
+        _lib.check(ctx.lib.qsb_debug_rng(ctx.handle, case["seed"] & ((1 << 64) - 1), case["shot"], 6, _lib.ptr(out)))
+        assert list(out) == case["uniforms"]
+
+
+@pytest.mark.parametrize("eng", ["resident", "stream"])
+def test_ff_suite_histograms_bit_exact(golden, eng):
+    with engine(eng):
+        for name, case in golden("ff_suite.json").items():
+            b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
+            assert sim.sample(b, 1024, 1234).counts == case["hist_1024_seed1234"], name
+
+
+@pytest.mark.parametrize("eng", ["resident", "stream"])
+def test_ff_suite_trajectories(golden, eng):
+    with engine(eng):
+        for name, case in golden("ff_suite.json").items():
+            b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
+            for rec in case["shots"][:32]:
+                rng = sim.RngStream.for_shot(1234, rec["shot"])
+                trace = []
+                store, st = sim.run_trajectory(b, rng, trace)
+                assert store.key() == rec["key"], (name, rec["shot"])
+                assert [[t[2], t[1]] for t in trace] == rec["trace"]
+                assert_state(st.amps, cvec(rec["state"]), 1e-10)
+                # rng advanced by exactly the uniforms consumed
+                ref = sim.RngStream.for_shot(1234, rec["shot"])
+                for _ in rec["uniforms"]:
+                    ref.uniform()
+                assert (rng.s0, rng.s1, rng.s2, rng.s3) == (ref.s0, ref.s1, ref.s2, ref.s3)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("eng", ["auto", "stream"])
+def test_static_statevectors_and_expval(golden, prec, eng):
+    with engine(eng):
+        for case in golden("static.json"):
+            k = ir.kernel_from_json(case["kernel"])
+            st = sim.statevector(ir.bind(k, case["values"]), precision=prec)
+            assert_state(st.amps, cvec(case["state"]), TOL[prec])
+            assert abs(st.norm() - case["norm"]) <= TOL[prec]
+            for word, val in case["expval"]:
+                assert abs(sim.expval_pauli(st, word) - val) <= 4 * TOL[prec], word
+
+
+def test_static_sampling_bit_exact(golden):
+    for case in golden("static_sampling.json"):
+        b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
+        assert sim.sample(b, case["shots"], case["seed"]).counts == case["counts"]
+
+
+@pytest.mark.parametrize("eng", ["resident", "stream"])
+def test_dynamic_random_circuits(golden, eng):
+    with engine(eng):
+        for case in golden("dynamic.json"):
+            b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
+            if case["counts_512"] is not None:
+                assert sim.sample(b, 512, case["seed"]).counts == case["counts_512"]
+            for rec in case["shots"]:
+                rng = sim.RngStream.for_shot(case["seed"], rec["shot"])
+                if "error" in rec:
+                    with pytest.raises(DegenerateNorm):
+                        sim.run_trajectory(b, rng)
+                    continue
+                trace = []
+                store, st = sim.run_trajectory(b, rng, trace)
+                assert store.key() == rec["key"]
+                assert [[t[2], t[1]] for t in trace] == rec["trace"]
+                if "state" in rec:
+                    assert_state(st.amps, cvec(rec["state"]), 1e-10)
+
+
+@pytest.mark.parametrize("eng", ["resident", "stream"])
+def test_predrawn_streams(golden, eng):
+    with engine(eng):
+        for case in golden("predrawn.json"):
+            b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
+            vals = np.array([case["values"]])
+            if "error" in case["record"]:
+                with pytest.raises(DegenerateNorm):
+                    sim.sample_words(b, 1, 0, predrawn=vals)
+                continue
+            words, tape = sim.sample_words(b, 1, 0, predrawn=vals)
+            assert tape.keys(words) == [case["record"]["key"]]
+            # the per-op path with an arbitrary uniform() object
+            store, st = sim.run_trajectory(b, P.PredrawnStream(case["values"]))
+            assert store.key() == case["record"]["key"]
+            assert_state(st.amps, cvec(case["record"]["state"]), 1e-10)
+
+
+@pytest.mark.parametrize("eng", ["resident", "stream"])
+def test_twins(golden, eng):
+    t = golden("twins.json")
+    with engine(eng):
+        b = ir.bind(ir.kernel_from_json(t["dyn8"]["kernel"]), [])
+        assert sim.sample(b, 1024, 1234).counts == t["dyn8"]["counts_1024"]
+        for rec in t["dyn8"]["shots"][:8]:
+            store, st = sim.run_trajectory(b, sim.RngStream.for_shot(1234, rec["shot"]))
+            assert store.key() == rec["key"]
+            if "state" in rec:
+                assert_state(st.amps, cvec(rec["state"]), 1e-10)
+        b = ir.bind(ir.kernel_from_json(t["rdc10"]["kernel"]), [])
+        for rec in t["rdc10"]["shots"]:
+            store, st = sim.run_trajectory(b, sim.RngStream.for_shot(1234, rec["shot"]))
+            assert store.key() == rec["key"]
+            if "state" in rec:
+                assert_state(st.amps, cvec(rec["state"]), 1e-10)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_vqe_observe(golden, prec):
+    v = golden("twins.json")["vqe6"]
+    k = ir.kernel_from_json(v["kernel"])
+    ham = [(c, w) for c, w in v["hamiltonian"]]
+    e, terms = sim.observe(k, ham, v["points"], precision=prec, return_terms=True)
+    scale = sum(abs(c) for c, _ in ham)
+    assert np.max(np.abs(e - np.array(v["energies"]))) <= TOL[prec] * scale
+    assert np.max(np.abs(terms - np.array(v["per_term"]))) <= 4 * TOL[prec]
+
+
+def test_dyn20_first_shots_bit_exact(golden):
+    """The headline workload (cfg 2) itself: per-shot keys of the first shots vs the
+    reference, and the consumed-uniform count."""
+    _, k = workloads.dyn_circuit()
+    b = ir.bind(k, [])
+    recs = golden("twins.json")["dyn20"]["shots"]
+    words, tape = sim.sample_words(b, len(recs), 1234)
+    assert tape.keys(words) == [r["key"] for r in recs]
+    for rec in recs:
+        rng = sim.RngStream.for_shot(1234, rec["shot"])
+        trace = []
+        store, st = sim.run_trajectory(b, rng, trace)
+        assert store.key() == rec["key"]
+        assert [[t[2], t[1]] for t in trace] == rec["trace"]
+        assert abs(st.norm() - 1.0) < 1e-10
+
+
+def test_rdc_state_vs_oracle_c128_and_c64():
+    """Down-scaled RDC (cfg 4 twin): final state of one trajectory, streaming engine."""
+    _, k = workloads.rdc_circuit(n=16, depth=40, every=20, seed=30200)
+    b = ir.bind(k, [])
+    rs, ref = P.trajectory(b, P.PortRng.for_shot(1234, 0))
+    for prec in ("c128", "c64"):
+        store, st = sim.run_trajectory(b, sim.RngStream.for_shot(1234, 0), precision=prec)
+        assert store.key() == rs.key()
+        assert_state(st.amps, ref.amps, TOL[prec])
+
+
+def test_batch_and_run_invariance():
+    """Histograms do not depend on the device batch size and repeat bit-identically."""
+    _, k = workloads.dyn_circuit(n=14, layers=10, every=5, nmeas=3, seed=11)
+    b = ir.bind(k, [])
+    base = sim.sample(b, 600, 77).counts
+    with option("batch", 64, 0):
+        assert sim.sample(b, 600, 77).counts == base
+    assert sim.sample(b, 600, 77).counts == base
+    ref = P.sample_counts(b, 60, 77)
+    assert sim.sample(b, 60, 77).counts == ref
+
+
+def test_tile_sizes_agree():
+    _, k = workloads.dyn_circuit(n=15, layers=10, every=5, nmeas=3, seed=12)
+    b = ir.bind(k, [])
+    want = P.trajectory_keys(b, 5, 0, 12)
+    for tq in (6, 9, 12):
+        with option("tile_qubits", tq, 0):
+            words, tape = sim.sample_words(b, 12, 5)
+            assert tape.keys(words) == want, tq
+
+
+def test_per_op_api_matches_reference_semantics():
+    from paper_2604_11599_b200.ir import Gate
+
+    st = sim.StateVector.zero(2)
+    sim.apply_gate(st, Gate("x", (), (0,), ()))
+    sim.apply_gate(st, Gate("x", (), (1,), ((0, 1),)))
+    np.testing.assert_allclose(st.amps, [0, 0, 0, 1], atol=1e-15)
+    st = sim.StateVector.zero(1)
+    sim.apply_gate(st, Gate("h", (), (0,), ()))
+    assert abs(sim.expval_pauli(st, "X") - 1.0) < 1e-12
+    outs = {sim.measure(sim.apply_gate(sim.StateVector.zero(1), Gate("h", (), (0,), ())), 0,
+                        sim.RngStream.for_shot(3, s)) for s in range(40)}
+    assert outs == {0, 1}
+    st = sim.StateVector.zero(1)
+    sim.apply_gate(st, Gate("x", (), (0,), ()))
+    sim.reset(st, 0, sim.RngStream(0))
+    np.testing.assert_allclose(st.amps, [1, 0], atol=1e-15)
+    # host edits of .amps are honoured by the next device op
+    st = sim.StateVector.zero(1)
+    a = st.amps
+    a[:] = [0, 1]
+    sim.apply_gate(st, Gate("x", (), (0,), ()))
+    np.testing.assert_allclose(st.amps, [1, 0], atol=1e-15)
+    with pytest.raises(BadPauliString):
+        sim.expval_pauli(st, "ZZ")
+    with pytest.raises(BadPauliString):
+        sim.expval_pauli(st, "Q")
+
+
+def test_errors():
+    _, k = workloads.ff_teleport()
+    b = ir.bind(k, [])
+    with pytest.raises(SimError):
+        sim.sample(b, 0, 1)
+    with pytest.raises(DynamicCircuit):
+        sim.statevector(b)
+    deg = ir.Kernel(1, [("q", 1)], [], [("c", 1)], [ir.Gate("rx", (2e-9,), (0,), ()), ir.Measure(0, ("c", 0))])
+    with pytest.raises(DegenerateNorm):
+        sim.sample_words(ir.bind(deg, []), 1, 0, predrawn=np.array([[0.0]]))
+
+
+def test_empty_and_no_bits():
+    k = ir.Kernel(1, [("q", 1)], [], [], [ir.Gate("h", (), (0,), ())])
+    assert sim.sample(ir.bind(k, []), 50, 1).counts == {"": 50}
+    k0 = ir.Kernel(0, [], [], [], [])
+    st = sim.statevector(ir.bind(k0, []))
+    np.testing.assert_allclose(st.amps, [1.0])
+
+
+def test_qft_matches_dft():
+    n = 12
+    body = [ir.Gate("x", (), (0,), ())]
+    for j in reversed(range(n)):
+        body.append(ir.Gate("h", (), (j,), ()))
+        for q in reversed(range(j)):
+            body.append(ir.Gate("p", (math.pi / (1 << (j - q)),), (j,), ((q, 1),)))
+    for i in range(n // 2):
+        body.append(ir.Gate("swap", (), (i, n - 1 - i), ()))
+    k = ir.Kernel(n, [("q", n)], [], [], body)
+    for eng in ("auto", "stream"):
+        with engine(eng):
+            st = sim.statevector(ir.bind(k, []))
+            j = np.arange(1 << n)
+            want = np.exp(2j * math.pi * j / (1 << n)) / math.sqrt(1 << n)
+            fid = abs(np.vdot(st.amps, want)) ** 2
+            assert fid > 1 - 1e-10
