@@ -1,0 +1,308 @@
+"""Benchmark: BASELINE.json configs[1] -- DYN20 dynamic circuit, batched trajectories.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one batch of B trajectories of DYN20 (20 qubits, 40 layers of u + cx,
+8 rounds of 4 x {measure, conditional x, reset}: 1180 gates + 64 draws per shot),
+each shot its own RNG stream RngStream.for_shot(1234, global_shot).  N ranks
+(torchrun, one process per GPU) run disjoint shot ranges -- no collective on the
+data path ("scaling": "weak"); the histogram merge is host-side.
+
+value  : shots/s over all ranks, device time (CUDA events on the library's stream,
+         max over ranks), states resident in HBM (B x 16 MiB >> 126 MB L2).
+e2e    : the same shots through the public API `sim.sample(bound, B, seed)`
+         (host wall clock, includes parameter upload, key download, histogram).
+roofline: the fused pass kernel (k_pass): algorithmic bytes 2 * 2^n * 16 B per state
+         per pass (1x for the first, write-only pass) / its CUDA-event time.
+--impl reference: the CPU oracle port (oracle/sim_port.py, a numpy restatement of the
+         reference simulator, pinned bit-exact to it) on the host cores, one process
+         per core, a bounded sample of DYN20 shots per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+SEED = 1234
+METRIC = "shots/s on the DYN20 dynamic circuit (20q, 1180 gates + 32 measure + 32 reset per shot, batched trajectories)"
+WORKLOAD = "DYN20: BASELINE configs[1], 20-qubit dynamic circuit, 10^5 batched trajectories"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        loaded = [r for r in self.rows if (num(r[7]) or 0) > 0] or self.rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(self.rows[0][1]),
+                "reasons": sorted(reasons), "samples": len(self.rows), "samples_under_load": len(loaded),
+                "power_w_max": max((num(r[2]) or 0) for r in self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port, one shot per worker process
+# ---------------------------------------------------------------------------
+
+
+def _cpu_shot(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sys.path.insert(0, REPO)
+    from oracle import sim_port as P
+    from paper_2604_11599_b200 import ir, workloads
+
+    shot, n, layers = args
+    _, k = workloads.dyn_circuit(n=n, layers=layers)
+    b = ir.bind(k, [])
+    t0 = time.perf_counter()
+    store, _ = P.trajectory(b, P.PortRng.for_shot(SEED, shot))
+    return store.key(), time.perf_counter() - t0
+
+
+def cpu_baseline(steps: int, warmup: int, shots_per_step: int | None = None) -> dict:
+    """Oracle port on all host cores (process pool, 1 BLAS thread each)."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    per = shots_per_step or cores
+    ctx = mp.get_context("spawn")
+    env_before = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    times = []
+    shot = 0
+    with ctx.Pool(processes=min(cores, per)) as pool:
+        for step in range(warmup + steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_shot, [(shot + i, 20, 40) for i in range(per)])
+            dt = time.perf_counter() - t0
+            shot += per
+            if step >= warmup:
+                times.append(dt)
+    if env_before is None:
+        os.environ.pop("OPENBLAS_NUM_THREADS", None)
+    total = sum(times)
+    return {"value": per * len(times) / total, "unit": "shots/s", "cores": min(cores, per), "kind": "port",
+            "sample": f"{per * len(times)} DYN20 shots ({per} per step, one per process, numpy oracle port "
+                      f"oracle/sim_port.py, OPENBLAS_NUM_THREADS=1), {total:.1f} s",
+            "ms_per_step": 1000 * total / len(times)}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.steps, args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "shots/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "qubits": 20, "seed": SEED},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "shots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2604_11599_b200 import _lib, ir, sim, workloads
+
+    ctx = _lib.context(local)
+    _, kernel = workloads.dyn_circuit()
+    bound = ir.bind(kernel, [])
+    B = args.batch
+    prec = args.precision
+    tape = sim.compile_tape(kernel, local)  # compile once (excluded from timing, like lower())
+    h2d_bytes = 8  # the step's seed / shot offset; DYN20 has no parameters
+    d2h_bytes = B * tape.nwords * 8 + B * 4
+
+    def step_shots(step):  # disjoint global shot ranges per (step, rank)
+        return (step * world + rank) * B
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(local)
+
+    # warm-up
+    for w in range(args.warmup):
+        sim.sample_words(bound, B, SEED, shot_begin=step_shots(w), precision=prec, device=local)
+    # timed device region
+    barrier()
+    dev_ms, pass_ms, pass_bytes, launches, gate_updates, ties, passes = 0.0, 0.0, 0.0, 0, 0, 0, 0
+    with ClockSampler(local) as clocks:
+        for s in range(args.steps):
+            sim.sample_words(bound, B, SEED, shot_begin=step_shots(args.warmup + s), precision=prec, device=local)
+            st = ctx.stats()
+            dev_ms += st["total_ms"]
+            pass_ms += st["pass_ms"]
+            pass_bytes += st["pass_bytes"]
+            launches += st["kernel_launches"]
+            gate_updates += st["gate_updates"]
+            ties += st["tie_band"]
+            passes += st["passes"]
+        barrier()
+    # e2e through the public API (host wall clock)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    hists = []
+    for s in range(e2e_steps):
+        hists.append(sim.sample(bound, B, SEED, precision=prec, device=local))
+    torch.cuda.synchronize(local)
+    e2e_s = time.perf_counter() - t0
+
+    t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    g = torch.tensor([gate_updates, ties, launches], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(g, op=dist.ReduceOp.SUM)
+    dev_ms_max, e2e_max = t.tolist()
+    gate_updates_all, ties_all, launches_all = g.tolist()
+    shots_total = B * args.steps * world
+    value = shots_total / (dev_ms_max / 1000.0)
+    e2e_value = B * e2e_steps * world / e2e_max
+    if rank == 0:
+        peaks, which = _peaks()
+        achieved = pass_bytes / (pass_ms / 1000.0) / 1e9 if pass_ms > 0 else None
+        traffic = None
+        prof = os.path.join(REPO, "profiles", "pass_kernel_traffic.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "shots/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": dev_ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64" if prec == "c128" else "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "qubits": 20, "batch_per_gpu": B, "shots_per_step": B * world,
+                       "precision": "complex128" if prec == "c128" else "complex64", "seed": SEED,
+                       "l2": f"inputs larger than L2: {B} x 16 MiB states per GPU",
+                       "engine": "streaming (fused passes + decide)", "tile_qubits": ctx.stats()["tile_qubits"]},
+            "gate_updates_per_s": gate_updates_all / (dev_ms_max / 1000.0),
+            "tie_band_decisions": int(ties_all),
+            "passes_per_step": passes / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": traffic,
+                         "kernel": "k_pass (fused gate pass)", "peak_kind": which,
+                         "algorithmic_bytes_per_step": pass_bytes / args.steps,
+                         "pass_ms_per_step": pass_ms / args.steps},
+            "e2e": {"value": e2e_value, "unit": "shots/s", "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": d2h_bytes, "api": "paper_2604_11599_b200.sim.sample"},
+            "gpu_launches": int(launches_all),
+            "clocks": clocks.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(1, 0)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=4096, help="trajectories per GPU per step")
+    ap.add_argument("--precision", choices=["c128", "c64"], default="c128")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -103,8 +103,12 @@ typedef struct {
   int64_t tie_band;          /* measure decisions with |u - p1| < 1e-12 (c128) / 1e-6 (c64) */
   int32_t engine;            /* 0 resident (state on chip), 1 streaming (state in HBM)    */
   int32_t tile_qubits;       /* k of the fused passes                                     */
+  int32_t jit_passes;        /* passes run by NVRTC-specialised kernels                   */
+  int32_t jit_compiled;      /* of those, compiled (not loaded from the cache) for this tape */
+  double jit_compile_ms;     /* one-time specialisation cost of the tape's plan           */
 } qsb_stats;
 
+#ifndef QSB_JIT /* the NVRTC prelude of the specialised kernels needs only the types */
 /* ---- library / context ---------------------------------------------------- */
 const char* qsb_last_error(void);
 int32_t qsb_abi_version(void);
@@ -179,9 +183,23 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
                     const uint64_t* xmask, const uint64_t* zmask, const int32_t* ny,
                     const double* coef, int32_t nterms, double* energies_out, double* term_out);
 
+/* host-only planner summary (no device needed): builds the streaming plan of a tape
+ * for tile_qubits / low_qubits / reg_bits and writes
+ * out[0..7] = {passes, phases, pass gates, regions, descriptor gates, epilogue passes,
+ *              max phases per pass, register-blocked (1) or shared-memory (0) kernel}.   */
+int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                         int32_t tile_qubits, int32_t low_qubits, int32_t reg_bits, int64_t* out);
+
+/* host-only: generate and NVRTC-compile (no device needed, nothing loaded) the
+ * specialised pass kernels of a tape's streaming plan; returns QSB_OK or QSB_ERR_ARG
+ * with the compiler log in qsb_last_error().  out[0] = kernels, out[1] = milliseconds. */
+int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                         int32_t precision, double* out);
+
 /* debug / known-answer hook: the first `count` uniforms of RngStream.for_shot(seed, shot)
  * drawn by the DEVICE generator (pins the on-device RNG to sim.py:54-72).              */
 int32_t qsb_debug_rng(qsb_ctx ctx, uint64_t seed, int64_t shot, int32_t count, double* out);
+#endif /* QSB_JIT */
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,9 @@ class Stats(ctypes.Structure):
         ("tie_band", ctypes.c_int64),
         ("engine", ctypes.c_int32),
         ("tile_qubits", ctypes.c_int32),
+        ("jit_passes", ctypes.c_int32),
+        ("jit_compiled", ctypes.c_int32),
+        ("jit_compile_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -102,6 +105,8 @@ _SIGS = {
     "qsb_sample_static": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P]),
     "qsb_observe": (_I32, [_P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P, _P]),
     "qsb_debug_rng": (_I32, [_P, _U64, _I64, _I32, _P]),
+    "qsb_plan_summary": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "qsb_jit_selftest": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

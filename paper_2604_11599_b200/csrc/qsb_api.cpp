@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "qsb_jit.h"
 #include "qsb_launch.h"
 #include "qsb_plan.h"
 
@@ -55,7 +56,11 @@ struct DevBuf {
 
 struct PlanDev {
   StreamPlan plan;
-  DevBuf gates, rops, guard_gates;
+  DevBuf gates, rops, guard_gates, phases, phase_gates;
+  std::vector<JitKernel> jit;  // NVRTC-specialised kernel per pass (empty: generic kernel)
+  std::string jit_error;
+  int jit_compiled = 0, jit_cached = 0;
+  double jit_ms = 0;
 };
 
 }  // namespace
@@ -66,7 +71,7 @@ struct qsb_ctx_s {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<cudaEvent_t> pass_events;
-  int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1;
+  int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace;
   qsb_stats last{};
 };
@@ -105,7 +110,7 @@ size_t amp_bytes(int c64) { return c64 ? 8 : 16; }
 
 int tile_qubits(qsb_ctx ctx, int c64) {
   if (ctx->opt_tile > 0) return (int)std::min<int64_t>(ctx->opt_tile, kMaxTile);
-  return c64 ? 13 : 12;  // 64 KiB of amplitudes per CTA
+  return 12;  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA
 }
 int low_qubits(int c64) { return c64 ? 5 : 4; }  // 256-byte contiguous runs
 
@@ -127,15 +132,19 @@ int upload_tape_device(qsb_tape tp) {
   return QSB_OK;
 }
 
-int get_plan(qsb_tape tp, int k, int lowq, PlanDev** out) {
-  int key = k * 64 + lowq;
+int reg_bits(int c64) { return 4; }
+
+int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
+  const int c64 = lowq == 5 ? 1 : 0;
+  const bool want_jit = tp->ctx->opt_jit && tp->info.n >= tp->ctx->opt_jit_min;
+  int key = ((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0);
   auto it = tp->plans.find(key);
   if (it != tp->plans.end()) {
     *out = it->second.get();
     return QSB_OK;
   }
   auto pd = std::make_unique<PlanDev>();
-  std::string e = build_stream_plan(tp->info, k, lowq, pd->plan);
+  std::string e = build_stream_plan(tp->info, k, lowq, rb, swizzle_bits(lowq == 5), pd->plan);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   StreamPlan& P = pd->plan;
   QSB_CUDA(pd->gates.ensure(std::max<size_t>(1, P.gates.size()) * sizeof(PassGate)));
@@ -147,6 +156,17 @@ int get_plan(qsb_tape tp, int k, int lowq, PlanDev** out) {
   QSB_CUDA(pd->guard_gates.ensure(std::max<size_t>(1, P.guard_gates.size()) * sizeof(int32_t)));
   QSB_CUDA(cudaMemcpy(pd->guard_gates.p, P.guard_gates.data(), P.guard_gates.size() * sizeof(int32_t),
                       cudaMemcpyHostToDevice));
+  QSB_CUDA(pd->phases.ensure(std::max<size_t>(1, P.phases.size()) * sizeof(PhaseDesc)));
+  if (!P.phases.empty())
+    QSB_CUDA(cudaMemcpy(pd->phases.p, P.phases.data(), P.phases.size() * sizeof(PhaseDesc), cudaMemcpyHostToDevice));
+  QSB_CUDA(pd->phase_gates.ensure(std::max<size_t>(1, P.phase_gates.size()) * sizeof(PhaseGate)));
+  if (!P.phase_gates.empty())
+    QSB_CUDA(cudaMemcpy(pd->phase_gates.p, P.phase_gates.data(), P.phase_gates.size() * sizeof(PhaseGate),
+                        cudaMemcpyHostToDevice));
+  if (want_jit && P.rb) {
+    pd->jit_error = jit_build(tp->info, P, c64, pd->jit, &pd->jit_ms, &pd->jit_compiled, &pd->jit_cached);
+    if (!pd->jit_error.empty()) pd->jit.clear();  // generic kernel for every pass
+  }
   *out = pd.get();
   tp->plans[key] = std::move(pd);
   return QSB_OK;
@@ -250,6 +270,8 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   a.n = t.n;
   a.c64 = r.c64;
   a.gates = r.pd->gates.as<PassGate>();
+  a.phases = P.rb ? r.pd->phases.as<PhaseDesc>() : nullptr;
+  a.phase_gates = r.pd->phase_gates.as<PhaseGate>();
   a.mats = r.mats;
   a.mat_stride = r.mat_stride;
   a.ctl = ctx->ctl.as<TrajCtl>();
@@ -288,7 +310,10 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
     if (s.type == 0) {
       const PassDesc& pd = P.passes[s.index];
       cudaEventRecord(ctx->pass_events[2 * s.index], ctx->stream);
-      QSB_CUDA(launch_pass(a, pd, ctx->stream));
+      if (s.index < (int)r.pd->jit.size() && r.pd->jit[s.index].kern)
+        QSB_CUDA(jit_launch(r.pd->jit[s.index], a, pd, ctx->stream));
+      else
+        QSB_CUDA(launch_pass(a, pd, ctx->stream));
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
       r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
       r.passes++;
@@ -352,6 +377,14 @@ int finish_stats(qsb_ctx ctx, float total_ms, double pass_ms, double pass_bytes,
   ctx->last.engine = engine;
   ctx->last.tile_qubits = k;
   return QSB_OK;
+}
+
+void note_jit(qsb_ctx ctx, const PlanDev* pd) {
+  int n = 0;
+  for (const JitKernel& k : pd->jit) n += k.kern ? 1 : 0;
+  ctx->last.jit_passes = n;
+  ctx->last.jit_compiled = pd->jit_compiled;
+  ctx->last.jit_compile_ms = pd->jit_ms;
 }
 
 int check_sticky() {
@@ -426,6 +459,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "batch") ctx->opt_batch = value;
   else if (k == "resident_max_qubits") ctx->opt_resident_max = value;
   else if (k == "engine") ctx->opt_engine = value;  // -1 auto, 0 resident, 1 streaming
+  else if (k == "jit") ctx->opt_jit = value;        // NVRTC per-pass kernels (1) or generic kernel (0)
+  else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "release_scratch") {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
@@ -713,6 +748,9 @@ int32_t qsb_tape_destroy(qsb_tape tp) {
       kv.second->gates.release();
       kv.second->rops.release();
       kv.second->guard_gates.release();
+      kv.second->phases.release();
+      kv.second->phase_gates.release();
+      jit_release(kv.second->jit);
     }
   }
   delete tp;
@@ -781,7 +819,7 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
     if (rc) return rc;
     int64_t B = pick_batch(ctx, t, pd->plan, c64, shot_count);
     QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
@@ -809,6 +847,7 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
     rc = check_sticky();
     if (rc) return rc;
     finish_stats(ctx, ms, pass_ms, pass_bytes, passes, decides, launches, 1, pd->plan.k);
+    note_jit(ctx, pd);
   }
   int worst = QSB_OK;
   for (int64_t i = 0; i < shot_count; ++i) {
@@ -894,7 +933,7 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
     if (rc) return rc;
     QSB_CUDA(ctx->state.ensure(amp_bytes(c64) << t.n));
     StreamRun r{tp, pd, c64, 1, ctx->state.p, mats, mstride, seed, shot, d_pre, npredrawn, 0, d_trace, max_trace,
@@ -918,6 +957,7 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
     QSB_CUDA(cudaMemcpy(d_draws, &c.draws, sizeof(int32_t), cudaMemcpyHostToDevice));
     finish_stats(ctx, ms, pass_ms_sum(ctx, pd->plan.passes.size()), r.pass_bytes, r.passes, r.decides, r.launches + 1,
                  1, pd->plan.k);
+    note_jit(ctx, pd);
   }
   QSB_CUDA(cudaMemcpy(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords, cudaMemcpyDeviceToHost));
   int32_t nt2[2] = {0, 0};
@@ -974,7 +1014,7 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
     return QSB_OK;
   }
   PlanDev* pd;
-  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
   if (rc) return rc;
   StreamRun r{tp, pd, c64, 1, out->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
   rc = run_stream(ctx, r);
@@ -984,6 +1024,7 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
   if (rc) return rc;
   finish_stats(ctx, ms, pass_ms_sum(ctx, pd->plan.passes.size()), r.pass_bytes, r.passes, r.decides, r.launches, 1,
                pd->plan.k);
+    note_jit(ctx, pd);
   return QSB_OK;
 }
 
@@ -1048,7 +1089,7 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
   RunTimer timer(ctx);
   PlanDev* pd;
-  int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), &pd);
+  int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
   if (rc) return rc;
   int64_t B = pick_batch(ctx, t, pd->plan, c64, npoints);
   QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
@@ -1097,6 +1138,7 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   rc = check_sticky();
   if (rc) return rc;
   finish_stats(ctx, ms, pass_ms, pass_bytes, passes, decides, launches, 1, pd->plan.k);
+    note_jit(ctx, pd);
   return QSB_OK;
 }
 
@@ -1113,5 +1155,47 @@ extern "C" int32_t qsb_debug_rng(qsb_ctx ctx, uint64_t seed, int64_t shot, int32
   qsb::launch_debug_rng(seed, shot, count, ctx->misc.as<double>(), ctx->stream);
   QSB_CUDA(cudaMemcpyAsync(out, ctx->misc.p, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
   QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return QSB_OK;
+}
+
+extern "C" int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                                    int32_t tile_qubits, int32_t low_qubits, int32_t reg_bits, int64_t* out) {
+  TapeInfo t;
+  std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  StreamPlan P;
+  e = build_stream_plan(t, tile_qubits, low_qubits, reg_bits, swizzle_bits(low_qubits == 5), P);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  int64_t epi = 0, maxph = 0;
+  for (const PassDesc& pd : P.passes) {
+    epi += pd.epi;
+    maxph = std::max<int64_t>(maxph, pd.phase_count);
+  }
+  out[0] = (int64_t)P.passes.size();
+  out[1] = (int64_t)P.phases.size();
+  out[2] = (int64_t)P.gates.size();
+  out[3] = (int64_t)P.regions.size();
+  out[4] = P.descriptor_gates;
+  out[5] = epi;
+  out[6] = maxph;
+  out[7] = P.rb ? 1 : 0;
+  return QSB_OK;
+}
+
+extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits,
+                                    int32_t nparams, int32_t precision, double* out) {
+  const int c64 = precision == QSB_C64 ? 1 : 0;
+  TapeInfo t;
+  std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  StreamPlan P;
+  e = build_stream_plan(t, 12, c64 ? 5 : 4, 4, swizzle_bits(c64), P);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  int nk = 0;
+  double ms = 0;
+  e = jit_compile_only(t, P, c64, &nk, &ms);
+  out[0] = nk;
+  out[1] = ms;
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
   return QSB_OK;
 }

@@ -1,10 +1,14 @@
 // Device helpers: complex arithmetic on interleaved amplitudes, the gate-matrix
 // builder for ParamRef angles, and the 2x2 update rules per gate class.
 #pragma once
+#ifndef QSB_JIT
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include "qsb_internal.h"
+#else
+#define CUDART_PI 3.1415926535897931e+0
+#endif
 
 namespace qsb {
 

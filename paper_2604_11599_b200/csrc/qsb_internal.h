@@ -11,10 +11,12 @@
 //   mats   : [slots or 1][nmat][8] 2x2 gate matrices (host-built for literal angles,
 //            device-built from params for ParamRef angles)
 #pragma once
+#ifndef QSB_JIT  // the NVRTC prelude (gen_prelude.py) inlines these files without system headers
 #include <cstdint>
 #include <cstddef>
 
 #include "../../include/qsb.h"
+#endif
 
 #ifdef __CUDACC__
 #define QSB_HD __host__ __device__ __forceinline__
@@ -81,7 +83,49 @@ struct PassGate {
   int32_t pad;
 };
 
+// Register-blocked execution of one pass (k_pass_reg): the tile lives in swizzled
+// shared memory; a phase maps r "register" tile positions R onto each thread's 2^r
+// registers and the other k - r positions onto the thread index, applies every gate
+// of the phase in registers, and writes back.  Phases change R (a remap through
+// shared memory) only when the next gate targets a position outside R.
+constexpr int kMaxRegBits = 5;
+enum PhaseKind : int32_t {
+  PK_DENSE = 0,   // target jt in R (2x2 general)
+  PK_XPERM = 1,   // x on jt in R
+  PK_ANTI = 2,    // y on jt in R
+  PK_DIAG_R = 3,  // diagonal, target jt in R
+  PK_DIAG_T = 4,  // diagonal, target tile position tp outside R (per-thread factor)
+  PK_DIAG_G = 5,  // diagonal, target outside the tile (per-CTA factor)
+  PK_SWAP_R = 6,  // swap of jt, jt2 both in R
+  // assigned on the device when the gate is staged, from the matrix values:
+  PK_DENSE_REAL = 7,  // all entries real (h, ry): 8 FMA per pair instead of 16
+  PK_DENSE_RX = 8,    // real diagonal, imaginary off-diagonal (rx): 8 FMA per pair
+  PK_SKIP = 9,        // guard off or out-of-tile control unsatisfied for this CTA
+};
+constexpr int kMaxPassGates = 256;  // gates staged in shared memory per pass
+
+struct PhaseGate {
+  int32_t kind;
+  int32_t jt, jt2;     // register-index bits of the targets
+  int32_t tp;          // PK_DIAG_T: tile position; PK_DIAG_G: global qubit
+  uint32_t cmR, cvR;   // controls on register bits (j space)
+  uint32_t cmT, cvT;   // controls on thread-mapped tile positions (checked on the thread base)
+  uint64_t gcm, gcv;   // controls outside the tile (logical qubit masks)
+  int32_t guard, mat;
+  int32_t diag_one0, pad;
+};
+
+struct PhaseDesc {
+  int32_t gate_begin, gate_count;
+  int32_t nt;                      // thread bits (k - r)
+  int32_t pad;
+  int8_t tpos[16];                 // thread bit i -> tile position
+  uint16_t soff[1 << kMaxRegBits]; // swizzled tile slot of register j (XOR with the thread base slot)
+};
+
 struct PassDesc {
+  int32_t phase_begin, phase_count;  // register-blocked phases (k_pass_reg); 0 = shared-memory kernel
+  int32_t pgate_begin, pgate_count;  // the phases' gates (contiguous in StreamPlan::phase_gates)
   uint64_t smask;       // tile qubits S (always includes the low `lowq` qubits)
   uint64_t clear_before;// frame bits cleared by earlier passes since the last decide
   uint64_t mmask;       // measured qubits of the next region (epilogue marginal)
@@ -124,6 +168,36 @@ struct TrajCtl {
   int32_t draws;         // uniforms consumed (pre-drawn streams)
   int32_t pad;
   int64_t gates;         // executed Gate ops (logical gate updates)
+};
+
+// kernel arguments of the streaming engine (passed by value)
+struct StreamArgs {
+  void* state;
+  int32_t n;
+  int32_t c64;
+  const PassGate* gates;
+  const PhaseDesc* phases;
+  const PhaseGate* phase_gates;
+  const double* mats;
+  int64_t mat_stride;
+  TrajCtl* ctl;
+  uint64_t* bits;
+  int32_t nwords;
+  int32_t gwords;
+  uint32_t* guards;
+  double* partial;
+  int64_t partial_stride;   // doubles per slot
+  int64_t slots;
+  // decide
+  const DevOp* region_ops;
+  const double* predrawn;
+  int32_t predrawn_stride;
+  int32_t ntiles_log2;
+  int64_t predrawn_slot0;   // global slot index of slot 0 (row of predrawn)
+  unsigned long long* tie_count;
+  int64_t* trace_out;
+  int32_t max_trace;
+  int32_t* ntrace_out;
 };
 
 QSB_HD uint64_t insert_zero(uint64_t v, int pos) {

@@ -1,0 +1,400 @@
+// NVRTC specialisation of the fused passes.
+//
+// The generic register-blocked kernel (qsb_pass_reg.cu) dispatches every gate through
+// a switch on (kind, target register bit, controls).  Each switch join forces the
+// compiler to shuffle the 16 register amplitudes back into canonical registers:
+// measured on B200, IMAD/MOV made up ~44% of the issued instructions against ~25%
+// FP64.  Here every pass of a compiled tape becomes its own kernel whose phases are
+// straight-line code: targets and register-bit controls are compile-time constants
+// (an x is a register renaming, a controlled gate touches only the matching pairs),
+// thread-bit controls become selects, and only guarded gates keep a (CTA-uniform)
+// branch.  Matrices still come from the per-CTA shared-memory staging, so ParamRef
+// tapes (one matrix set per VQE point) use the same kernels.  Each phase is a
+// __noinline__ function (phases communicate through shared memory only), which keeps
+// ptxas time linear in the number of phases.
+//
+// Kernels are compiled once per tape (compile-once, like the reference's kir.lower),
+// in parallel, and cached on disk by source hash.
+#include "qsb_jit.h"
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <thread>
+
+#include "qsb_pass_common.cuh"
+
+namespace qsb {
+
+#include "jit_prelude.inc"
+
+namespace {
+
+struct Nvrtc {
+  void* h = nullptr;
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  bool ok = false;
+};
+
+Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so"}) {
+      n.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (n.h) break;
+    }
+    if (!n.h) return;
+    n.create = (decltype(n.create))dlsym(n.h, "nvrtcCreateProgram");
+    n.compile = (decltype(n.compile))dlsym(n.h, "nvrtcCompileProgram");
+    n.cubin_size = (decltype(n.cubin_size))dlsym(n.h, "nvrtcGetCUBINSize");
+    n.cubin = (decltype(n.cubin))dlsym(n.h, "nvrtcGetCUBIN");
+    n.log_size = (decltype(n.log_size))dlsym(n.h, "nvrtcGetProgramLogSize");
+    n.log = (decltype(n.log))dlsym(n.h, "nvrtcGetProgramLog");
+    n.destroy = (decltype(n.destroy))dlsym(n.h, "nvrtcDestroyProgram");
+    n.ok = n.create && n.compile && n.cubin_size && n.cubin && n.log_size && n.log && n.destroy;
+  });
+  return n;
+}
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+std::string cache_dir() {
+  const char* e = getenv("QSB_JIT_CACHE");
+  std::string d = e && *e ? e : "/tmp/qsb_jit_cache";
+  mkdir(d.c_str(), 0755);
+  return d;
+}
+
+const char* kOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-DQSB_JIT=1"};
+
+bool compile_one(const std::string& src, std::vector<char>& cubin, std::string& log) {
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) {
+    log = "libnvrtc not available";
+    return false;
+  }
+  nvrtcProgram prog;
+  if (nv.create(&prog, src.c_str(), "qsb_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    log = "nvrtcCreateProgram failed";
+    return false;
+  }
+  nvrtcResult rc = nv.compile(prog, (int)(sizeof(kOpts) / sizeof(kOpts[0])), kOpts);
+  size_t ls = 0;
+  nv.log_size(prog, &ls);
+  if (ls > 1) {
+    log.resize(ls);
+    nv.log(prog, &log[0]);
+  }
+  bool ok = rc == NVRTC_SUCCESS;
+  if (ok) {
+    size_t n = 0;
+    nv.cubin_size(prog, &n);
+    cubin.resize(n);
+    nv.cubin(prog, cubin.data());
+  }
+  nv.destroy(&prog);
+  return ok;
+}
+
+// ---------------------------------------------------------------------------
+// code generation
+// ---------------------------------------------------------------------------
+
+enum DenseVariant { DV_GEN, DV_REAL, DV_RX };
+
+DenseVariant dense_variant(const MatSrc& m) {
+  if (m.has_matrix) {
+    const double* x = m.mat;
+    if (x[1] == 0.0 && x[3] == 0.0 && x[5] == 0.0 && x[7] == 0.0) return DV_REAL;
+    if (x[1] == 0.0 && x[7] == 0.0 && x[2] == 0.0 && x[4] == 0.0) return DV_RX;
+    return DV_GEN;
+  }
+  if (m.base == QSB_G_H || m.base == QSB_G_RY) return DV_REAL;
+  if (m.base == QSB_G_RX) return DV_RX;
+  return DV_GEN;
+}
+
+const char* kHelpers = R"(
+__device__ __forceinline__ A CM(R mr, R mi, A a) { return qsb::cmul<R>(mr, mi, a); }
+__device__ __forceinline__ void G_GEN(A& a0, A& a1, const R* m) {
+  A b0 = qsb::cmac2<R>(m[0], m[1], a0, m[2], m[3], a1);
+  A b1 = qsb::cmac2<R>(m[4], m[5], a0, m[6], m[7], a1);
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_REAL(A& a0, A& a1, const R* m) {
+  A b0 = qsb::mk<R>(fma(m[0], a0.x, m[2] * a1.x), fma(m[0], a0.y, m[2] * a1.y));
+  A b1 = qsb::mk<R>(fma(m[4], a0.x, m[6] * a1.x), fma(m[4], a0.y, m[6] * a1.y));
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_RX(A& a0, A& a1, const R* m) {
+  A b0 = qsb::mk<R>(fma(m[0], a0.x, -m[3] * a1.y), fma(m[0], a0.y, m[3] * a1.x));
+  A b1 = qsb::mk<R>(fma(m[6], a1.x, -m[5] * a0.y), fma(m[6], a1.y, m[5] * a0.x));
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_ANTI(A& a0, A& a1, const R* m) {
+  A b0 = qsb::cmul<R>(m[2], m[3], a1);
+  A b1 = qsb::cmul<R>(m[4], m[5], a0);
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_DIAG(A& a0, A& a1, const R* m) {
+  a0 = qsb::cmul<R>(m[0], m[1], a0);
+  a1 = qsb::cmul<R>(m[6], m[7], a1);
+}
+)";
+
+void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
+                const PhaseDesc& ph, int sb) {
+  o << "__device__ __noinline__ void ph" << ph_index
+    << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
+       "const int tid) {\n";
+  o << "  const uint32_t base = 0u";
+  for (int i = 0; i < ph.nt; ++i) o << " | ((((uint32_t)tid >> " << i << ") & 1u) << " << (int)ph.tpos[i] << ")";
+  o << ";\n  const uint32_t sb = base ^ swz[base >> " << sb << "];\n";
+  for (int j = 0; j < 16; ++j) o << "  A v" << j << " = tile[sb ^ " << ph.soff[j] << "u];\n";
+  for (int gl = 0; gl < ph.gate_count; ++gl) {
+    const int gidx = ph.gate_begin + gl;
+    const PhaseGate& q = P.phase_gates[gidx];
+    const int gi = gidx - pd.pgate_begin;
+    const MatSrc& ms = t.mats[q.mat];
+    const bool need_skip = q.guard >= 0 || q.gcm != 0 || q.kind == PK_DIAG_G;
+    o << "  {  // gate " << gi << " kind " << q.kind << "\n";
+    if (need_skip) o << "  if (sg[" << gi << "].kind != " << (int)PK_SKIP << ") {\n";
+    o << "  const R* m = sg[" << gi << "].m;\n";
+    const bool thr = q.cmT != 0;
+    if (thr) o << "  const bool c = (base & " << q.cmT << "u) == " << q.cvT << "u;\n";
+    auto sel_pair = [&](int j0, int j1, const char* fn) {
+      if (!thr) {
+        o << "  " << fn << "(v" << j0 << ", v" << j1 << ", m);\n";
+      } else {
+        o << "  { A t0 = v" << j0 << ", t1 = v" << j1 << "; " << fn << "(t0, t1, m); v" << j0 << " = c ? t0 : v" << j0
+          << "; v" << j1 << " = c ? t1 : v" << j1 << "; }\n";
+      }
+    };
+    auto scale = [&](int j, const char* dr, const char* di) {
+      if (!thr) o << "  v" << j << " = CM(" << dr << ", " << di << ", v" << j << ");\n";
+      else o << "  v" << j << " = c ? CM(" << dr << ", " << di << ", v" << j << ") : v" << j << ";\n";
+    };
+    switch (q.kind) {
+      case PK_DENSE:
+      case PK_XPERM:
+      case PK_ANTI:
+      case PK_DIAG_R: {
+        const int b = 1 << q.jt;
+        const char* fn = "G_GEN";
+        if (q.kind == PK_DENSE) {
+          DenseVariant dv = dense_variant(ms);
+          fn = dv == DV_REAL ? "G_REAL" : dv == DV_RX ? "G_RX" : "G_GEN";
+        } else if (q.kind == PK_ANTI) {
+          fn = "G_ANTI";
+        } else if (q.kind == PK_DIAG_R) {
+          fn = "G_DIAG";
+        }
+        for (int j = 0; j < 16; ++j) {
+          if (j & b) continue;
+          if (((uint32_t)j & q.cmR) != q.cvR) continue;
+          const int j1 = j | b;
+          if (q.kind == PK_XPERM) {
+            if (!thr) o << "  { A x = v" << j << "; v" << j << " = v" << j1 << "; v" << j1 << " = x; }\n";
+            else
+              o << "  { A x = v" << j << "; v" << j << " = c ? v" << j1 << " : v" << j << "; v" << j1 << " = c ? x : v"
+                << j1 << "; }\n";
+          } else if (q.kind == PK_DIAG_R && q.diag_one0) {
+            scale(j1, "m[6]", "m[7]");
+          } else {
+            sel_pair(j, j1, fn);
+          }
+        }
+      } break;
+      case PK_DIAG_T: {
+        o << "  const bool bt = (base >> " << q.tp << ") & 1u;\n";
+        o << "  const R dr = bt ? m[6] : m[0], di = bt ? m[7] : m[1];\n";
+        for (int j = 0; j < 16; ++j)
+          if (((uint32_t)j & q.cmR) == q.cvR) scale(j, "dr", "di");
+      } break;
+      case PK_DIAG_G: {
+        for (int j = 0; j < 16; ++j)
+          if (((uint32_t)j & q.cmR) == q.cvR) scale(j, "m[0]", "m[1]");
+      } break;
+      default:
+        o << "  // unsupported kind\n";
+        break;
+    }
+    if (need_skip) o << "  }\n";
+    o << "  }\n";
+  }
+  for (int j = 0; j < 16; ++j) o << "  tile[sb ^ " << ph.soff[j] << "u] = v" << j << ";\n";
+  o << "}\n";
+}
+
+}  // namespace
+
+bool jit_available() { return nvrtc().ok; }
+
+std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
+  const PassDesc& pd = P.passes[pass];
+  const int sb = c64 ? 4 : 3;
+  std::ostringstream o;
+  for (const char* part : kJitPreludeParts) o << part;
+  o << "\ntypedef " << (c64 ? "float" : "double") << " R;\ntypedef " << (c64 ? "float2" : "double2") << " A;\n";
+  o << kHelpers;
+  for (int i = 0; i < pd.phase_count; ++i) {
+    const PhaseDesc& ph = P.phases[pd.phase_begin + i];
+    if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb);
+  }
+  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
+  o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+  o << "  qsb::PassCtx<R> cx;\n";
+  o << "  if (!qsb::pass_begin<R, 4>(a, pd, smem_raw, cx)) return;\n";
+  for (int i = 0; i < pd.phase_count; ++i) {
+    const PhaseDesc& ph = P.phases[pd.phase_begin + i];
+    if (ph.nt >= 0) o << "  ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";
+    else o << "  qsb::pass_swap<R, " << sb << ">(cx, cx.sg[" << (ph.gate_begin - pd.pgate_begin) << "]);\n";
+    o << "  __syncthreads();\n";
+  }
+  o << "  qsb::pass_end<R, " << sb << ">(a, pd, cx);\n}\n";
+  return o.str();
+}
+
+std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vector<JitKernel>& out,
+                      double* compile_ms, int* compiled, int* cached) {
+  auto t0 = std::chrono::steady_clock::now();
+  out.assign(P.passes.size(), JitKernel());
+  *compiled = *cached = 0;
+  if (!P.rb) return "";
+  if (!jit_available()) return "libnvrtc not available";
+  const std::string dir = cache_dir();
+  struct Job {
+    int pass;
+    std::string src, path;
+    std::vector<char> cubin;
+    std::string log;
+    bool ok = false, from_cache = false;
+  };
+  std::vector<Job> jobs;
+  for (int i = 0; i < (int)P.passes.size(); ++i) {
+    if (P.passes[i].phase_count == 0) continue;
+    Job j;
+    j.pass = i;
+    j.src = jit_source(t, P, i, c64);
+    std::string key = j.src;
+    for (const char* opt : kOpts) key += opt;
+    char name[64];
+    snprintf(name, sizeof(name), "/%016llx.cubin", (unsigned long long)fnv1a(key));
+    j.path = dir + name;
+    std::ifstream f(j.path, std::ios::binary);
+    if (f) {
+      j.cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+      j.ok = j.from_cache = !j.cubin.empty();
+    }
+    jobs.push_back(std::move(j));
+  }
+  std::atomic<size_t> next(0);
+  unsigned nthreads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+  std::vector<std::thread> pool;
+  for (unsigned w = 0; w < nthreads; ++w)
+    pool.emplace_back([&] {
+      for (size_t i = next++; i < jobs.size(); i = next++) {
+        Job& j = jobs[i];
+        if (j.ok) continue;
+        j.ok = compile_one(j.src, j.cubin, j.log);
+        if (j.ok) {
+          std::string tmp = j.path + ".tmp" + std::to_string(i);
+          std::ofstream f(tmp, std::ios::binary);
+          f.write(j.cubin.data(), (std::streamsize)j.cubin.size());
+          f.close();
+          rename(tmp.c_str(), j.path.c_str());
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (Job& j : jobs) {
+    if (!j.ok) {
+      jit_release(out);
+      return "NVRTC failed for pass " + std::to_string(j.pass) + ": " + j.log.substr(0, 2000);
+    }
+    cudaLibrary_t lib;
+    cudaError_t e = cudaLibraryLoadData(&lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) {
+      jit_release(out);
+      return std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+    }
+    cudaKernel_t k;
+    e = cudaLibraryGetKernel(&k, lib, "qsb_jit_pass");
+    if (e != cudaSuccess) {
+      cudaLibraryUnload(lib);
+      jit_release(out);
+      return std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+    }
+    JitKernel& jk = out[j.pass];
+    jk.lib = (void*)lib;
+    jk.kern = (void*)k;
+    jk.smem = pass_reg_smem(c64, P.passes[j.pass], 4);
+    e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
+    if (e != cudaSuccess) {
+      jit_release(out);
+      return std::string("cudaFuncSetAttribute (jit): ") + cudaGetErrorString(e);
+    }
+    if (j.from_cache) (*cached)++;
+    else (*compiled)++;
+  }
+  *compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return "";
+}
+
+std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, int* kernels, double* ms) {
+  auto t0 = std::chrono::steady_clock::now();
+  *kernels = 0;
+  for (int i = 0; i < (int)P.passes.size(); ++i) {
+    if (P.passes[i].phase_count == 0) continue;
+    std::vector<char> cubin;
+    std::string log;
+    const std::string src = jit_source(t, P, i, c64);
+    if (const char* d = getenv("QSB_JIT_DUMP")) {  // debug: keep the generated sources
+      std::ofstream f(std::string(d) + "/pass" + std::to_string(i) + ".cu");
+      f << src;
+    }
+    if (!compile_one(src, cubin, log)) return "pass " + std::to_string(i) + ": " + log;
+    (*kernels)++;
+  }
+  *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return "";
+}
+
+cudaError_t jit_launch(const JitKernel& jk, const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
+  StreamArgs aa = a;
+  PassDesc pp = pd;
+  void* args[] = {(void*)&aa, (void*)&pp};
+  dim3 grid((unsigned)(1ull << (a.n - pd.k)), (unsigned)a.slots);
+  dim3 block((unsigned)(1u << (pd.k - 4)));
+  return cudaLaunchKernel((const void*)jk.kern, grid, block, args, jk.smem, s);
+}
+
+void jit_release(std::vector<JitKernel>& ks) {
+  for (JitKernel& k : ks)
+    if (k.lib) cudaLibraryUnload((cudaLibrary_t)k.lib);
+  ks.clear();
+}
+
+}  // namespace qsb

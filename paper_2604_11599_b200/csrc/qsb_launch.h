@@ -75,33 +75,9 @@ void launch_mats_prep(const MatSrc* src, int nmat, const double* params, int npa
 void launch_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards, int gwords, int64_t slots,
                      uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, cudaStream_t s);
 
-struct StreamArgs {
-  void* state;
-  int32_t n;
-  int32_t c64;
-  const PassGate* gates;
-  const double* mats;
-  int64_t mat_stride;
-  TrajCtl* ctl;
-  uint64_t* bits;
-  int32_t nwords;
-  int32_t gwords;
-  uint32_t* guards;
-  double* partial;
-  int64_t partial_stride;   // doubles per slot
-  int64_t slots;
-  // decide
-  const DevOp* region_ops;
-  const double* predrawn;
-  int32_t predrawn_stride;
-  int32_t ntiles_log2;
-  int64_t predrawn_slot0;   // global slot index of slot 0 (row of predrawn)
-  unsigned long long* tie_count;
-  int64_t* trace_out;
-  int32_t max_trace;
-  int32_t* ntrace_out;
-};
 cudaError_t launch_pass(const StreamArgs& a, const PassDesc& pd, cudaStream_t s);
+// register-blocked variant (qsb_pass_reg.cu), used when the pass has phases
+cudaError_t launch_pass_reg(const StreamArgs& a, const PassDesc& pd, cudaStream_t s);
 cudaError_t launch_decide(const StreamArgs& a, const RegionDesc& rd, cudaStream_t s);
 void launch_count_gates(const StreamArgs& a, const int32_t* guard_gates, int nguards, int64_t unguarded,
                         unsigned long long* out, cudaStream_t s);

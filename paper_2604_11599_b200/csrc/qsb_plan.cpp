@@ -25,6 +25,26 @@ namespace qsb {
 
 static int popc(uint64_t v) { return __builtin_popcountll(v); }
 
+// Swizzle vectors: tile position p >= sb contributes V[p] to the low sb slot bits.
+// Every nonzero vector appears at most twice (sb = 3) / once (sb = 4), so any set of
+// >= 7 (resp. >= 8) thread-mapped positions spans all sb dimensions and a phase can
+// always give its 2^sb consecutive threads distinct bank groups.
+static const uint32_t kV3[16] = {1, 2, 4, 3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7, 1, 2};
+static const uint32_t kV4[16] = {1, 2, 4, 8, 3, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 1};
+
+int swizzle_bits(int c64) { return c64 ? 4 : 3; }
+
+uint32_t swizzle_hi(uint32_t hi, int sb) {
+  const uint32_t* V = sb == 3 ? kV3 : kV4;
+  uint32_t s = 0;
+  for (int p = sb; hi; ++p, hi >>= 1)
+    if (hi & 1) s ^= V[p];
+  return s;
+}
+
+static uint32_t swz_slot(uint32_t l, int sb) { return l ^ swizzle_hi(l >> sb, sb); }
+static uint32_t swz_vec(int p, int sb) { return p < sb ? (1u << p) : (sb == 3 ? kV3[p] : kV4[p]); }
+
 static int gate_class_of(int base) {
   switch (base) {
     case QSB_G_X: return GC_XPERM;
@@ -184,11 +204,145 @@ bool is_prefix(const std::vector<int>& a, const std::vector<int>& b) {
 
 struct Planner {
   const TapeInfo& t;
-  int k, lowq;
+  int k, lowq, rb;
+  int swz_bits_ = 3;
   StreamPlan& P;
   std::vector<RegionBuild> regions;
 
-  Planner(const TapeInfo& t_, int k_, int lowq_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), P(p) {}
+  Planner(const TapeInfo& t_, int k_, int lowq_, int rb_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), rb(rb_), P(p) {}
+
+  // Split one pass's gates into register-blocked phases (greedy first fit: a gate
+  // joins the phase if its non-diagonal targets fit in the rb register positions and
+  // none of its tile positions is blocked by an earlier deferred gate).
+  void build_phases(PassDesc& pd) {
+    const int sb = swz_bits_;
+    const int nt = k - rb;
+    pd.phase_begin = (int)P.phases.size();
+    pd.pgate_begin = (int)P.phase_gates.size();
+    std::vector<int> rem;
+    for (int i = 0; i < pd.gate_count; ++i) rem.push_back(pd.gate_begin + i);
+    while (!rem.empty()) {
+      if (P.gates[rem[0]].gclass == GC_SWAP) {  // swaps run as their own shared-memory phase
+        const PassGate& g = P.gates[rem[0]];
+        PhaseDesc ph{};
+        ph.nt = -1;
+        ph.gate_begin = (int)P.phase_gates.size();
+        ph.gate_count = 1;
+        PhaseGate q{};
+        q.kind = PK_SWAP_R;
+        q.tp = g.lt;
+        q.jt2 = g.lt2;
+        q.cmT = g.lcm;
+        q.cvT = g.lcv;
+        q.gcm = g.gcm;
+        q.gcv = g.gcv;
+        q.guard = g.guard;
+        q.mat = g.mat;
+        P.phase_gates.push_back(q);
+        P.phases.push_back(ph);
+        rem.erase(rem.begin());
+        continue;
+      }
+      uint32_t R = 0, blocked = 0;
+      std::vector<int> take, rest;
+      for (int gi : rem) {
+        const PassGate& g = P.gates[gi];
+        uint32_t touched = g.lcm;
+        if (g.gclass != GC_DIAG_GLOBAL) touched |= 1u << g.lt;
+        if (g.gclass == GC_SWAP) touched |= 1u << g.lt2;
+        if ((touched & blocked) || g.gclass == GC_SWAP) {
+          rest.push_back(gi);
+          blocked |= touched;
+          continue;
+        }
+        uint32_t need = 0;
+        if (g.gclass == GC_DENSE || g.gclass == GC_XPERM || g.gclass == GC_ANTI) need = 1u << g.lt;
+        need &= ~R;
+        if (popc(R | need) <= rb) {
+          R |= need;
+          take.push_back(gi);
+        } else {
+          rest.push_back(gi);
+          blocked |= touched;
+        }
+      }
+      for (int p = 0; p < k && popc(R) < rb; ++p) R |= 1u << p;
+      PhaseDesc ph{};
+      ph.nt = nt;
+      int rpos[kMaxRegBits], rj[32];
+      int nr = 0;
+      for (int p = 0; p < k; ++p) {
+        rj[p] = -1;
+        if (R >> p & 1) {
+          rpos[nr] = p;
+          rj[p] = nr++;
+        }
+      }
+      // thread positions: first sb positions with independent swizzle vectors
+      std::vector<int> tp, others;
+      uint32_t basis[8] = {0};
+      for (int p = 0; p < k; ++p) {
+        if (R >> p & 1) continue;
+        uint32_t v = swz_vec(p, sb);
+        for (int b = sb - 1; b >= 0 && v; --b)
+          if (v >> b & 1) {
+            if (basis[b]) v ^= basis[b];
+            else {
+              basis[b] = v;
+              break;
+            }
+          }
+        if (v && (int)tp.size() < sb) tp.push_back(p);
+        else others.push_back(p);
+      }
+      for (int p : others) tp.push_back(p);
+      for (int i = 0; i < nt; ++i) ph.tpos[i] = (int8_t)tp[i];
+      for (int j = 0; j < (1 << rb); ++j) {
+        uint32_t off = 0;
+        for (int b = 0; b < rb; ++b)
+          if (j >> b & 1) off |= 1u << rpos[b];
+        ph.soff[j] = (uint16_t)swz_slot(off, sb);
+      }
+      ph.gate_begin = (int)P.phase_gates.size();
+      for (int gi : take) {
+        const PassGate& g = P.gates[gi];
+        PhaseGate q{};
+        q.guard = g.guard;
+        q.mat = g.mat;
+        q.diag_one0 = g.diag_one0;
+        q.gcm = g.gcm;
+        q.gcv = g.gcv;
+        switch (g.gclass) {
+          case GC_DENSE: q.kind = PK_DENSE; q.jt = rj[g.lt]; break;
+          case GC_XPERM: q.kind = PK_XPERM; q.jt = rj[g.lt]; break;
+          case GC_ANTI: q.kind = PK_ANTI; q.jt = rj[g.lt]; break;
+          case GC_SWAP: q.kind = PK_SWAP_R; q.jt = rj[g.lt]; q.jt2 = rj[g.lt2]; break;
+          case GC_DIAG:
+            if (rj[g.lt] >= 0) { q.kind = PK_DIAG_R; q.jt = rj[g.lt]; }
+            else { q.kind = PK_DIAG_T; q.tp = g.lt; }
+            break;
+          default: q.kind = PK_DIAG_G; q.tp = g.gq; break;
+        }
+        for (uint32_t m = g.lcm; m; m &= m - 1) {
+          int p = __builtin_ctz(m);
+          uint32_t v = (g.lcv >> p) & 1;
+          if (rj[p] >= 0) {
+            q.cmR |= 1u << rj[p];
+            q.cvR |= v << rj[p];
+          } else {
+            q.cmT |= 1u << p;
+            q.cvT |= v << p;
+          }
+        }
+        P.phase_gates.push_back(q);
+      }
+      ph.gate_count = (int)take.size();
+      P.phases.push_back(ph);
+      rem.swap(rest);
+    }
+    pd.phase_count = (int)P.phases.size() - pd.phase_begin;
+    pd.pgate_count = (int)P.phase_gates.size() - pd.pgate_begin;
+  }
 
   uint64_t low_mask() const { return lowq >= 64 ? ~0ull : ((1ull << lowq) - 1); }
 
@@ -238,6 +392,8 @@ struct Planner {
     pd.gate_count = (int)chosen.size();
     pd.region = epi_region;
     pd.epi = epi_region >= 0 ? 1 : 0;
+    pd.phase_begin = pd.phase_count = 0;
+    if (rb > 0 && pd.k - rb >= 5 && pd.k == k) build_phases(pd);
     P.passes.push_back(pd);
     P.steps.push_back({0, (int)P.passes.size() - 1});
   }
@@ -255,6 +411,10 @@ struct Planner {
       std::vector<int> chosen, rest;
       for (int gi : remaining) {
         const DevOp& d = t.dev[gi];
+        if ((int)chosen.size() == kMaxPassGates) {  // staging capacity of k_pass_reg
+          rest.push_back(gi);
+          continue;
+        }
         uint64_t tm = (1ull << d.t0) | (d.t1 >= 0 ? (1ull << d.t1) : 0);
         uint64_t touched = tm | d.cm;
         if (touched & blocked) {
@@ -435,14 +595,16 @@ struct Planner {
 
 }  // namespace
 
-std::string build_stream_plan(const TapeInfo& t, int k, int lowq, StreamPlan& out) {
+std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz, StreamPlan& out) {
   out = StreamPlan();
   k = std::max(1, std::min(k, std::min(t.n, kMaxTile)));
   lowq = std::max(0, std::min(lowq, k));
   out.k = k;
   out.lowq = lowq;
+  out.rb = (rb > 0 && k - rb >= 5) ? rb : 0;
   out.ntiles_log2 = t.n - k;
-  Planner pl(t, k, lowq, out);
+  Planner pl(t, k, lowq, out.rb, out);
+  pl.swz_bits_ = swz;
   return pl.run();
 }
 

@@ -27,10 +27,17 @@ struct Step {
   int index;
 };
 
+// shared-memory swizzle of the register-blocked pass kernel: slot(l) = l ^ V(l >> sb),
+// V linear; `sb` = 3 for 16-byte amplitudes, 4 for 8-byte ones.
+int swizzle_bits(int c64);
+uint32_t swizzle_hi(uint32_t hi, int sb);  // V applied to tile bits >= sb (hi = l >> sb)
+
 struct StreamPlan {
-  int k = 0, lowq = 0, ntiles_log2 = 0;
+  int k = 0, lowq = 0, ntiles_log2 = 0, rb = 0;
   std::vector<PassDesc> passes;
   std::vector<PassGate> gates;
+  std::vector<PhaseDesc> phases;
+  std::vector<PhaseGate> phase_gates;
   std::vector<RegionDesc> regions;
   std::vector<DevOp> region_ops;
   std::vector<Step> steps;
@@ -40,6 +47,8 @@ struct StreamPlan {
   int64_t descriptor_gates = 0;     // gates folded into decide regions
 };
 
-std::string build_stream_plan(const TapeInfo& t, int k, int lowq, StreamPlan& out);
+// rb = register bits of k_pass_reg (4 for complex128, 5 for complex64); phases are
+// built when k - rb >= 5 (at least one warp per tile), else the shared-memory kernel runs.
+std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz_bits, StreamPlan& out);
 
 }  // namespace qsb

@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kPT) k_pass(StreamArgs a, PassDesc pd) {
   }
 }
 
+
 // complex helpers on (re, im) doubles for the decide kernel
 struct Cd {
   double r, i;
@@ -435,6 +436,8 @@ cudaError_t launch_pass(const StreamArgs& a, const PassDesc& pd, cudaStream_t s)
   size_t smem = pass_smem(a.c64, pd);
   dim3 grid((unsigned)(1ull << (a.n - pd.k)), (unsigned)a.slots);
   cudaError_t e;
+  if (a.phases && (pd.phase_count > 0 || pd.gate_count == 0) && pd.k - 4 >= 5)
+    return launch_pass_reg(a, pd, s);
   if (a.c64) {
     e = cudaFuncSetAttribute(k_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
