@@ -21,6 +21,7 @@
 #include <nvrtc.h>
 #include <sys/stat.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -265,15 +266,14 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   }
   o << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-  o << "  qsb::PassCtx<R> cx;\n";
-  o << "  if (!qsb::pass_begin<R, 4>(a, pd, smem_raw, cx)) return;\n";
+  o << "  qsb::pass_persistent<R, 4>(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
-    if (ph.nt >= 0) o << "  ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";
-    else o << "  qsb::pass_swap<R, " << sb << ">(cx, cx.sg[" << (ph.gate_begin - pd.pgate_begin) << "]);\n";
-    o << "  __syncthreads();\n";
+    if (ph.nt >= 0) o << "    ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";
+    else o << "    qsb::pass_swap<R, " << sb << ">(cx, cx.sg[" << (ph.gate_begin - pd.pgate_begin) << "]);\n";
+    o << "    __syncthreads();\n";
   }
-  o << "  qsb::pass_end<R, " << sb << ">(a, pd, cx);\n}\n";
+  o << "  });\n}\n";
   return o.str();
 }
 
@@ -356,6 +356,11 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vect
       jit_release(out);
       return std::string("cudaFuncSetAttribute (jit): ") + cudaGetErrorString(e);
     }
+    int per_sm = 1, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, 1 << (P.passes[j.pass].k - 4), jk.smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    jk.max_grid = (int64_t)std::max(1, per_sm) * sms;
     if (j.from_cache) (*cached)++;
     else (*compiled)++;
   }
@@ -386,7 +391,8 @@ cudaError_t jit_launch(const JitKernel& jk, const StreamArgs& a, const PassDesc&
   StreamArgs aa = a;
   PassDesc pp = pd;
   void* args[] = {(void*)&aa, (void*)&pp};
-  dim3 grid((unsigned)(1ull << (a.n - pd.k)), (unsigned)a.slots);
+  const int64_t W = (int64_t)a.slots << (a.n - pd.k);
+  dim3 grid((unsigned)std::min<int64_t>(W, jk.max_grid));
   dim3 block((unsigned)(1u << (pd.k - 4)));
   return cudaLaunchKernel((const void*)jk.kern, grid, block, args, jk.smem, s);
 }

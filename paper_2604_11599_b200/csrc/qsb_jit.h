@@ -14,6 +14,7 @@ struct JitKernel {
   void* lib = nullptr;   // cudaLibrary_t
   void* kern = nullptr;  // cudaKernel_t
   size_t smem = 0;
+  int64_t max_grid = 148;  // resident CTAs (persistent kernel)
 };
 
 // true if libnvrtc could be loaded

@@ -12,6 +12,8 @@
 // pass regardless of how many gates it carries.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "qsb_launch.h"
 #include "qsb_pass_common.cuh"
 
@@ -82,59 +84,69 @@ __global__ void __launch_bounds__(256, 2) k_pass_reg(StreamArgs a, PassDesc pd) 
   constexpr int NR = 1 << RB;
   constexpr int SB = sizeof(R) == 8 ? 3 : 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PassCtx<R> cx;
-  if (!pass_begin<R, RB>(a, pd, smem_raw, cx)) return;
-  const int tid = cx.tid;
-  for (int ph = 0; ph < pd.phase_count; ++ph) {
-    const PhaseDesc* P = a.phases + pd.phase_begin + ph;
-    const int nt = P->nt;
-    if (nt < 0) {
-      pass_swap<R, SB>(cx, cx.sg[P->gate_begin - pd.pgate_begin]);
-      __syncthreads();
-      continue;
-    }
-    uint32_t base = 0;
-    for (int i = 0; i < nt; ++i) base |= (uint32_t)((tid >> i) & 1) << P->tpos[i];
-    const uint32_t sbase = swz_slot<SB>(cx.swz, base);
-    A v[NR];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) v[j] = cx.tile[sbase ^ P->soff[j]];
-    const int g0 = P->gate_begin - pd.pgate_begin, g1 = g0 + P->gate_count;
-    for (int gi = g0; gi < g1; ++gi) {
-      const SGate<R>& g = cx.sg[gi];
-      const int kind = g.kind;
-      if (kind == PK_SKIP) continue;
-      if ((base & g.cmT) != g.cvT) continue;
-      R m[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m[j] = g.m[j];
-      switch (kind) {
-        case PK_DENSE: ph_kind<R, NR, PK_DENSE>(g.jt, v, m, g.cmR, g.cvR); break;
-        case PK_DENSE_REAL: ph_kind<R, NR, PK_DENSE_REAL>(g.jt, v, m, g.cmR, g.cvR); break;
-        case PK_DENSE_RX: ph_kind<R, NR, PK_DENSE_RX>(g.jt, v, m, g.cmR, g.cvR); break;
-        case PK_XPERM: ph_kind<R, NR, PK_XPERM>(g.jt, v, m, g.cmR, g.cvR); break;
-        case PK_ANTI: ph_kind<R, NR, PK_ANTI>(g.jt, v, m, g.cmR, g.cvR); break;
-        case PK_DIAG_R: ph_kind<R, NR, PK_DIAG_R>(g.jt, v, m, g.cmR, g.cvR); break;
-        default: {  // PK_DIAG_T (per-thread factor) / PK_DIAG_G (per-CTA factor, resolved at staging)
-          R dr = m[0], di = m[1];
-          if (g.tp >= 0) {
-            const int b = (int)((base >> g.tp) & 1);
-            if (!b && g.jt) break;  // jt carries diag_one0
-            if (b) {
-              dr = m[6];
-              di = m[7];
-            }
-          }
-          if (g.cmR) ph_scale<R, NR, true>(v, dr, di, g.cmR, g.cvR);
-          else ph_scale<R, NR, false>(v, dr, di, 0, 0);
-        } break;
+  pass_persistent<R, RB>(a, pd, smem_raw, [&](const PassCtx<R>& cx) {
+    const int tid = cx.tid;
+    for (int ph = 0; ph < pd.phase_count; ++ph) {
+      const PhaseDesc* P = a.phases + pd.phase_begin + ph;
+      const int nt = P->nt;
+      if (nt < 0) {
+        pass_swap<R, SB>(cx, cx.sg[P->gate_begin - pd.pgate_begin]);
+        __syncthreads();
+        continue;
       }
-    }
+      uint32_t base = 0;
+      for (int i = 0; i < nt; ++i) base |= (uint32_t)((tid >> i) & 1) << P->tpos[i];
+      const uint32_t sbase = swz_slot<SB>(cx.swz, base);
+      A v[NR];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) cx.tile[sbase ^ P->soff[j]] = v[j];
-    __syncthreads();
+      for (int j = 0; j < NR; ++j) v[j] = cx.tile[sbase ^ P->soff[j]];
+      const int g0 = P->gate_begin - pd.pgate_begin, g1 = g0 + P->gate_count;
+      for (int gi = g0; gi < g1; ++gi) {
+        const SGate<R>& g = cx.sg[gi];
+        const int kind = g.kind;
+        if (kind == PK_SKIP) continue;
+        if ((base & g.cmT) != g.cvT) continue;
+        R m[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = g.m[j];
+        switch (kind) {
+          case PK_DENSE: ph_kind<R, NR, PK_DENSE>(g.jt, v, m, g.cmR, g.cvR); break;
+          case PK_DENSE_REAL: ph_kind<R, NR, PK_DENSE_REAL>(g.jt, v, m, g.cmR, g.cvR); break;
+          case PK_DENSE_RX: ph_kind<R, NR, PK_DENSE_RX>(g.jt, v, m, g.cmR, g.cvR); break;
+          case PK_XPERM: ph_kind<R, NR, PK_XPERM>(g.jt, v, m, g.cmR, g.cvR); break;
+          case PK_ANTI: ph_kind<R, NR, PK_ANTI>(g.jt, v, m, g.cmR, g.cvR); break;
+          case PK_DIAG_R: ph_kind<R, NR, PK_DIAG_R>(g.jt, v, m, g.cmR, g.cvR); break;
+          default: {  // PK_DIAG_T (per-thread factor) / PK_DIAG_G (per-CTA factor, resolved at staging)
+            R dr = m[0], di = m[1];
+            if (g.tp >= 0) {
+              const int b = (int)((base >> g.tp) & 1);
+              if (!b && g.jt) break;  // jt carries diag_one0
+              if (b) {
+                dr = m[6];
+                di = m[7];
+              }
+            }
+            if (g.cmR) ph_scale<R, NR, true>(v, dr, di, g.cmR, g.cvR);
+            else ph_scale<R, NR, false>(v, dr, di, 0, 0);
+          } break;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NR; ++j) cx.tile[sbase ^ P->soff[j]] = v[j];
+      __syncthreads();
+    }
+  });
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
   }
-  pass_end<R, SB>(a, pd, cx);
+  return sms;
 }
 
 template <typename R> cudaError_t launch_t(const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
@@ -142,8 +154,12 @@ template <typename R> cudaError_t launch_t(const StreamArgs& a, const PassDesc& 
   const size_t sm = pass_reg_smem(a.c64, pd, 4);
   cudaError_t e = cudaFuncSetAttribute(k_pass_reg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)(1ull << (a.n - pd.k)), (unsigned)a.slots);
-  k_pass_reg<R><<<grid, T, sm, s>>>(a, pd);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_reg<R>, T, sm);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t W = (int64_t)a.slots << (a.n - pd.k);
+  const int64_t grid = std::min<int64_t>(W, (int64_t)per_sm * num_sms());
+  k_pass_reg<R><<<(unsigned)grid, T, sm, s>>>(a, pd);
   return cudaGetLastError();
 }
 
