@@ -132,8 +132,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   const int64_t W = (int64_t)a.slots << ntl;
   const uint64_t qmask = (a.n >= 64) ? ~0ull : ((1ull << a.n) - 1);
 
-  auto prefetch = [&](int64_t w, A* dst) {
-    const PassItem it = pass_item(a, pd, w, ntl);
+  auto prefetch = [&](const PassItem& it, A* dst) {
     if (!it.alive) return;
     const A* st = reinterpret_cast<const A*>(a.state) + (it.slot << a.n);
     for (int l = tid; l < TL; l += T) {
@@ -149,8 +148,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     }
   };
 
-  auto prefetch_next_l2 = [&](int64_t w) {  // one 2^lowq-amplitude run per thread
-    const PassItem it = pass_item(a, pd, w, ntl);
+  auto prefetch_next_l2 = [&](const PassItem& it) {  // one 2^lowq-amplitude run per thread
     if (!it.alive || pd.init_zero) return;
     const A* st = reinterpret_cast<const A*>(a.state) + (it.slot << a.n);
     for (int h = tid; h < (TL >> pd.lowq); h += T)
@@ -158,23 +156,30 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   };
 
   int64_t w = blockIdx.x;
-  if (NB == 2 && w < W) prefetch(w, bufs);
+  PassItem cur;
+  cur.alive = false;
+  if (w < W) cur = pass_item(a, pd, w, ntl);
+  if (NB == 2 && w < W) prefetch(cur, bufs);
   cp_async_commit();
   int b = 0;
   for (; w < W; w += gridDim.x) {
     const int64_t wn = w + gridDim.x;
+    PassItem nxt;
+    nxt.alive = false;
+    if (wn < W) nxt = pass_item(a, pd, wn, ntl);
     if (NB == 2) {
-      if (wn < W) prefetch(wn, bufs + (b ^ 1) * TL);
+      if (wn < W) prefetch(nxt, bufs + (b ^ 1) * TL);
       cp_async_commit();
       cp_async_wait1();
     } else {
-      if (wn < W) prefetch_next_l2(wn);
-      prefetch(w, bufs);
+      if (wn < W) prefetch_next_l2(nxt);
+      prefetch(cur, bufs);
       cp_async_commit();
       cp_async_wait0();
     }
     __syncthreads();
-    const PassItem it = pass_item(a, pd, w, ntl);
+    const PassItem it = cur;
+    cur = nxt;
     A* tile = bufs + b * TL;
     if (it.alive) {
       if (it.pending) {  // collapse of the previous decide: projection + complex scale
@@ -245,9 +250,13 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
           for (int jj = 0; jj < ml; ++jj)
             if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
           double s = 0.0;
+          // members r = j, j + tp, ... deposited into free_mask by masked addition
+          // (x | ~mask) + d carries across the holes), in increasing order
+          const uint32_t inc = (uint32_t)pdep64((uint64_t)tp, free_mask);
+          uint32_t f = (uint32_t)pdep64((uint64_t)j, free_mask);
           for (int r = j; r < members; r += tp) {
-            uint32_t l = (uint32_t)pdep64((uint64_t)r, free_mask) | bpos;
-            s += norm2<R>(tile[swz_slot<SB>(swz, l)]);
+            s += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+            f = ((f | ~free_mask) + inc) & free_mask;
           }
           red[tid] = s;
           __syncthreads();
@@ -262,9 +271,10 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
             for (int jj = 0; jj < ml; ++jj)
               if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
             double s = 0.0;
+            uint32_t f = 0;
             for (int r = 0; r < members; ++r) {
-              uint32_t l = (uint32_t)pdep64((uint64_t)r, free_mask) | bpos;
-              s += norm2<R>(tile[swz_slot<SB>(swz, l)]);
+              s += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+              f = ((f | ~free_mask) + 1u) & free_mask;
             }
             out[bb] = s;
           }
