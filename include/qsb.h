@@ -199,6 +199,10 @@ int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32
 /* debug / known-answer hook: the first `count` uniforms of RngStream.for_shot(seed, shot)
  * drawn by the DEVICE generator (pins the on-device RNG to sim.py:54-72).              */
 int32_t qsb_debug_rng(qsb_ctx ctx, uint64_t seed, int64_t shot, int32_t count, double* out);
+
+/* measured FMA throughput of this device in TFLOP/s (fp64 for QSB_C128, fp32 for
+ * QSB_C64): the compute roofline denominator of the pass kernels.                     */
+int32_t qsb_debug_fma_peak(qsb_ctx ctx, int32_t precision, double* tflops);
 #endif /* QSB_JIT */
 
 #ifdef __cplusplus

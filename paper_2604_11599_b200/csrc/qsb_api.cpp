@@ -1146,6 +1146,14 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
 
 namespace qsb {
 void launch_debug_rng(uint64_t seed, int64_t shot, int count, double* out, cudaStream_t s);
+double measure_fma_peak(int c64, int num_sms, cudaStream_t s);
+}
+
+extern "C" int32_t qsb_debug_fma_peak(qsb_ctx ctx, int32_t precision, double* tflops) {
+  DeviceGuard g(ctx->device);
+  *tflops = qsb::measure_fma_peak(precision == QSB_C64 ? 1 : 0, ctx->num_sms, ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
 }
 
 extern "C" int32_t qsb_debug_rng(qsb_ctx ctx, uint64_t seed, int64_t shot, int32_t count, double* out) {

@@ -165,6 +165,53 @@ __device__ __forceinline__ void G_DIAG(A& a0, A& a1, const R* m) {
 }
 )";
 
+// Zero pattern of a dense matrix (bit i set: component m[i] is exactly zero), known at
+// code-generation time for literal matrices and, for ParamRef angles, from the base
+// (u: m00 = cos(theta/2) is real).
+uint32_t zero_mask(const MatSrc& m) {
+  uint32_t z = 0;
+  if (m.has_matrix) {
+    for (int i = 0; i < 8; ++i)
+      if (m.mat[i] == 0.0) z |= 1u << i;
+    return z;
+  }
+  if (m.base == QSB_G_U) return 1u << 1;
+  return 0;
+}
+
+// A dense 2x2 with statically-zero components dropped from cmac2's FMA chain.  The
+// chain keeps cmac2's association order, and the dropped terms are exact zeros, so
+// the result is bit-identical to the generic kernel's cmac2.
+std::string sparse_helper(uint32_t z) {
+  std::ostringstream o;
+  auto chain = [&](const char* out, const int* c, const char** x, const bool* neg) {
+    // terms innermost first: (c[i], x[i], neg[i])
+    std::string acc;
+    for (int i = 0; i < 4; ++i) {
+      if (z >> c[i] & 1) continue;
+      std::string coef = std::string(neg[i] ? "-" : "") + "m[" + std::to_string(c[i]) + "]";
+      if (acc.empty()) acc = coef + " * " + x[i];
+      else acc = "fma(" + coef + ", " + x[i] + ", " + acc + ")";
+    }
+    if (acc.empty()) acc = "(R)0";
+    o << "  " << out << " = " << acc << ";\n";
+  };
+  o << "__device__ __forceinline__ void G_S" << z << "(A& a0, A& a1, const R* m) {\n  A b0, b1;\n";
+  for (int r = 0; r < 2; ++r) {
+    const int o0 = 4 * r;  // m00 m01 (row 0) or m10 m11 (row 1)
+    int cre[4] = {o0 + 3, o0 + 2, o0 + 1, o0 + 0};
+    const char* xre[4] = {"a1.y", "a1.x", "a0.y", "a0.x"};
+    bool nre[4] = {true, false, true, false};
+    int cim[4] = {o0 + 3, o0 + 2, o0 + 1, o0 + 0};
+    const char* xim[4] = {"a1.x", "a1.y", "a0.x", "a0.y"};
+    bool nim[4] = {false, false, false, false};
+    chain(r ? "b1.x" : "b0.x", cre, xre, nre);
+    chain(r ? "b1.y" : "b0.y", cim, xim, nim);
+  }
+  o << "  a0 = b0; a1 = b1;\n}\n";
+  return o.str();
+}
+
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
                 const PhaseDesc& ph, int sb) {
   o << "__device__ __noinline__ void ph" << ph_index
@@ -203,10 +250,14 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
       case PK_ANTI:
       case PK_DIAG_R: {
         const int b = 1 << q.jt;
-        const char* fn = "G_GEN";
+        std::string fname = "G_GEN";
         if (q.kind == PK_DENSE) {
           DenseVariant dv = dense_variant(ms);
-          fn = dv == DV_REAL ? "G_REAL" : dv == DV_RX ? "G_RX" : "G_GEN";
+          const uint32_t z = zero_mask(ms);
+          fname = dv == DV_REAL ? "G_REAL" : dv == DV_RX ? "G_RX" : z ? "G_S" + std::to_string(z) : "G_GEN";
+        }
+        const char* fn = fname.c_str();
+        if (q.kind == PK_DENSE) {
         } else if (q.kind == PK_ANTI) {
           fn = "G_ANTI";
         } else if (q.kind == PK_DIAG_R) {
@@ -260,6 +311,19 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   for (const char* part : kJitPreludeParts) o << part;
   o << "\ntypedef " << (c64 ? "float" : "double") << " R;\ntypedef " << (c64 ? "float2" : "double2") << " A;\n";
   o << kHelpers;
+  {  // sparse dense-gate helpers used by this pass
+    std::vector<uint32_t> seen;
+    for (int g = pd.pgate_begin; g < pd.pgate_begin + pd.pgate_count; ++g) {
+      const PhaseGate& q = P.phase_gates[g];
+      if (q.kind != PK_DENSE) continue;
+      const MatSrc& ms = t.mats[q.mat];
+      if (dense_variant(ms) != DV_GEN) continue;
+      const uint32_t z = zero_mask(ms);
+      if (!z || std::find(seen.begin(), seen.end(), z) != seen.end()) continue;
+      seen.push_back(z);
+      o << sparse_helper(z);
+    }
+  }
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb);

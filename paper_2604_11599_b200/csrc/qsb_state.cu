@@ -321,4 +321,45 @@ __global__ void k_debug_rng(uint64_t seed, int64_t shot, int count, double* out)
 void launch_debug_rng(uint64_t seed, int64_t shot, int count, double* out, cudaStream_t s) {
   k_debug_rng<<<1, 1, 0, s>>>(seed, shot, count, out);
 }
+
+// FMA-throughput probe (8 independent chains per thread): the compute roofline of the
+// pass kernels, measured on the box instead of quoted from a datasheet.
+template <typename R> __global__ void k_fma_peak(R* out, int iters, R a, R b) {
+  R x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = (R)(threadIdx.x + i);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  R s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == (R)-1.2345) out[0] = s;  // keep the chains alive
+}
+
+double measure_fma_peak(int c64, int num_sms, cudaStream_t s) {
+  const int threads = 256, blocks = num_sms * 8, iters = 4096;
+  void* out = nullptr;
+  cudaMalloc(&out, 64);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, s);
+    if (c64) k_fma_peak<float><<<blocks, threads, 0, s>>>((float*)out, iters, 0.999f, 1e-7f);
+    else k_fma_peak<double><<<blocks, threads, 0, s>>>((double*)out, iters, 0.999, 1e-7);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * iters * (double)threads * blocks;
+  return flops / (best * 1e-3) / 1e12;  // TFLOP/s
+}
 }  // namespace qsb
