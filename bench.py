@@ -22,6 +22,7 @@ roofline: the fused pass kernel (k_pass): algorithmic bytes 2 * 2^n * 16 B per s
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -208,6 +209,10 @@ def run_ours(args) -> None:
     # timed device region
     barrier()
     dev_ms, pass_ms, pass_bytes, launches, gate_updates, ties, passes = 0.0, 0.0, 0.0, 0, 0, 0, 0
+    flops, jit_passes = 0.0, 0
+    fma_peak = ctypes.c_double()
+    _lib.check(ctx.lib.qsb_debug_fma_peak(ctx.handle, _lib.C64 if prec == "c64" else _lib.C128,
+                                          ctypes.byref(fma_peak)))
     with ClockSampler(local) as clocks:
         for s in range(args.steps):
             sim.sample_words(bound, B, SEED, shot_begin=step_shots(args.warmup + s), precision=prec, device=local)
@@ -219,6 +224,8 @@ def run_ours(args) -> None:
             gate_updates += st["gate_updates"]
             ties += st["tie_band"]
             passes += st["passes"]
+            flops += st["pass_flops"]
+            jit_passes = st["jit_passes"]
         barrier()
     # e2e through the public API (host wall clock)
     barrier()
@@ -247,7 +254,9 @@ def run_ours(args) -> None:
         prof = os.path.join(REPO, "profiles", "pass_kernel_traffic.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+                # ncu dram bytes per state-pass x the states one pass launch processes here
+                per_state = json.load(open(prof)).get("traffic_bytes_per_state_pass")
+                traffic = per_state * B if (per_state and prec == "c128") else None
             except Exception:
                 traffic = None
         line = {
@@ -275,6 +284,16 @@ def run_ours(args) -> None:
                          "kernel": "k_pass (fused gate pass)", "peak_kind": which,
                          "algorithmic_bytes_per_step": pass_bytes / args.steps,
                          "pass_ms_per_step": pass_ms / args.steps},
+            # the pass kernel's binding roof for complex128 is the FP64 FMA pipe, not HBM:
+            # executed floating-point work (FMA = 2) vs the FMA throughput probed on this GPU
+            "compute_roofline": {"bound": "fp64" if prec == "c128" else "fp32",
+                                 "achieved": flops / (pass_ms / 1000.0) / 1e12 if pass_ms > 0 else None,
+                                 "peak": fma_peak.value, "unit": "TFLOP/s",
+                                 "frac": (flops / (pass_ms / 1000.0) / 1e12 / fma_peak.value)
+                                 if pass_ms > 0 and fma_peak.value > 0 else None,
+                                 "peak_kind": "measured on this GPU (qsb_debug_fma_peak)",
+                                 "flops_per_step": flops / args.steps},
+            "jit_passes": jit_passes,
             "e2e": {"value": e2e_value, "unit": "shots/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes, "api": "paper_2604_11599_b200.sim.sample"},
             "gpu_launches": int(launches_all),

@@ -106,6 +106,7 @@ typedef struct {
   int32_t jit_passes;        /* passes run by NVRTC-specialised kernels                   */
   int32_t jit_compiled;      /* of those, compiled (not loaded from the cache) for this tape */
   double jit_compile_ms;     /* one-time specialisation cost of the tape's plan           */
+  double pass_flops;         /* floating-point operations (FMA = 2) of the pass kernels   */
 } qsb_stats;
 
 #ifndef QSB_JIT /* the NVRTC prelude of the specialised kernels needs only the types */

@@ -62,6 +62,7 @@ class Stats(ctypes.Structure):
         ("jit_passes", ctypes.c_int32),
         ("jit_compiled", ctypes.c_int32),
         ("jit_compile_ms", ctypes.c_double),
+        ("pass_flops", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

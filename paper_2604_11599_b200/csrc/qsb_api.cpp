@@ -58,6 +58,7 @@ struct PlanDev {
   StreamPlan plan;
   DevBuf gates, rops, guard_gates, phases, phase_gates;
   std::vector<JitKernel> jit;  // NVRTC-specialised kernel per pass (empty: generic kernel)
+  std::vector<double> pflops;  // floating-point operations per state of each pass
   std::string jit_error;
   int jit_compiled = 0, jit_cached = 0;
   double jit_ms = 0;
@@ -74,6 +75,7 @@ struct qsb_ctx_s {
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace;
   qsb_stats last{};
+  double run_flops = 0;  // floating-point work of the pass kernels in the current run
 };
 
 struct qsb_state_s {
@@ -163,6 +165,9 @@ int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
   if (!P.phase_gates.empty())
     QSB_CUDA(cudaMemcpy(pd->phase_gates.p, P.phase_gates.data(), P.phase_gates.size() * sizeof(PhaseGate),
                         cudaMemcpyHostToDevice));
+  pd->pflops.assign(P.passes.size(), 0.0);
+  for (size_t i = 0; i < P.passes.size(); ++i)
+    if (P.passes[i].phase_count) pd->pflops[i] = pass_flops(tp->info, P, (int)i);
   if (want_jit && P.rb) {
     pd->jit_error = jit_build(tp->info, P, c64, pd->jit, &pd->jit_ms, &pd->jit_compiled, &pd->jit_cached);
     if (!pd->jit_error.empty()) pd->jit.clear();  // generic kernel for every pass
@@ -316,6 +321,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
         QSB_CUDA(launch_pass(a, pd, ctx->stream));
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
       r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
+      ctx->run_flops += r.pd->pflops[s.index] * (double)r.slots;
       r.passes++;
       r.launches++;
       acc |= pd.smask;
@@ -372,6 +378,7 @@ int finish_stats(qsb_ctx ctx, float total_ms, double pass_ms, double pass_bytes,
   ctx->last.pass_ms = pass_ms;
   ctx->last.total_ms = total_ms;
   ctx->last.pass_bytes = pass_bytes;
+  ctx->last.pass_flops = ctx->run_flops;
   ctx->last.gate_updates = (int64_t)cnt[1];
   ctx->last.tie_band = (int64_t)cnt[0];
   ctx->last.engine = engine;
@@ -771,6 +778,7 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
   const TapeInfo& t = tp->info;
   const int c64 = precision == QSB_C64 ? 1 : 0;
   QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  ctx->run_flops = 0;
   RunTimer timer(ctx);
   const double* d_params = nullptr;
   int rc = upload_params(tp, params, 1, &d_params);
@@ -871,6 +879,7 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
   if (state_out && (state_out->n != t.n || state_out->c64 != c64))
     return fail(QSB_ERR_DIMENSION, "state_out shape / precision mismatch");
   QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  ctx->run_flops = 0;
   RunTimer timer(ctx);
   const double* d_params = nullptr;
   int rc = upload_params(tp, params, 1, &d_params);
@@ -983,6 +992,7 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
   DeviceGuard g(ctx->device);
   const int c64 = out->c64;
   QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  ctx->run_flops = 0;
   RunTimer timer(ctx);
   const double* d_params = nullptr;
   int rc = upload_params(tp, params, 1, &d_params);
@@ -1087,6 +1097,7 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   DeviceGuard g(ctx->device);
   const int c64 = precision == QSB_C64 ? 1 : 0;
   QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  ctx->run_flops = 0;
   RunTimer timer(ctx);
   PlanDev* pd;
   int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);

@@ -123,19 +123,6 @@ bool compile_one(const std::string& src, std::vector<char>& cubin, std::string& 
 // code generation
 // ---------------------------------------------------------------------------
 
-enum DenseVariant { DV_GEN, DV_REAL, DV_RX };
-
-DenseVariant dense_variant(const MatSrc& m) {
-  if (m.has_matrix) {
-    const double* x = m.mat;
-    if (x[1] == 0.0 && x[3] == 0.0 && x[5] == 0.0 && x[7] == 0.0) return DV_REAL;
-    if (x[1] == 0.0 && x[7] == 0.0 && x[2] == 0.0 && x[4] == 0.0) return DV_RX;
-    return DV_GEN;
-  }
-  if (m.base == QSB_G_H || m.base == QSB_G_RY) return DV_REAL;
-  if (m.base == QSB_G_RX) return DV_RX;
-  return DV_GEN;
-}
 
 const char* kHelpers = R"(
 __device__ __forceinline__ A CM(R mr, R mi, A a) { return qsb::cmul<R>(mr, mi, a); }
@@ -164,20 +151,6 @@ __device__ __forceinline__ void G_DIAG(A& a0, A& a1, const R* m) {
   a1 = qsb::cmul<R>(m[6], m[7], a1);
 }
 )";
-
-// Zero pattern of a dense matrix (bit i set: component m[i] is exactly zero), known at
-// code-generation time for literal matrices and, for ParamRef angles, from the base
-// (u: m00 = cos(theta/2) is real).
-uint32_t zero_mask(const MatSrc& m) {
-  uint32_t z = 0;
-  if (m.has_matrix) {
-    for (int i = 0; i < 8; ++i)
-      if (m.mat[i] == 0.0) z |= 1u << i;
-    return z;
-  }
-  if (m.base == QSB_G_U) return 1u << 1;
-  return 0;
-}
 
 // A dense 2x2 with statically-zero components dropped from cmac2's FMA chain.  The
 // chain keeps cmac2's association order, and the dropped terms are exact zeros, so

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <map>
+#include <cmath>
 #include <sstream>
 
 namespace qsb {
@@ -606,6 +607,62 @@ std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int sw
   Planner pl(t, k, lowq, out.rb, out);
   pl.swz_bits_ = swz;
   return pl.run();
+}
+
+DenseVariant dense_variant(const MatSrc& m) {
+  if (m.has_matrix) {
+    const double* x = m.mat;
+    if (x[1] == 0.0 && x[3] == 0.0 && x[5] == 0.0 && x[7] == 0.0) return DV_REAL;
+    if (x[1] == 0.0 && x[7] == 0.0 && x[2] == 0.0 && x[4] == 0.0) return DV_RX;
+    return DV_GEN;
+  }
+  if (m.base == QSB_G_H || m.base == QSB_G_RY) return DV_REAL;
+  if (m.base == QSB_G_RX) return DV_RX;
+  return DV_GEN;
+}
+
+uint32_t zero_mask(const MatSrc& m) {
+  uint32_t z = 0;
+  if (m.has_matrix) {
+    for (int i = 0; i < 8; ++i)
+      if (m.mat[i] == 0.0) z |= 1u << i;
+    return z;
+  }
+  if (m.base == QSB_G_U) return 1u << 1;  // m00 = cos(theta/2) is real
+  return 0;
+}
+
+double phase_gate_flops(const PhaseGate& q, const MatSrc& m) {
+  switch (q.kind) {
+    case PK_XPERM:
+    case PK_SWAP_R: return 0;
+    case PK_DENSE: {
+      DenseVariant dv = dense_variant(m);
+      if (dv != DV_GEN) return 12;
+      const uint32_t z = zero_mask(m);
+      double f = 0;
+      for (int r = 0; r < 2; ++r)
+        for (int comp = 0; comp < 2; ++comp) {
+          int terms = 0;
+          for (int i = 0; i < 4; ++i) terms += (z >> (4 * r + i) & 1) ? 0 : 1;
+          if (terms) f += 2.0 * (terms - 1) + 1.0;  // (terms-1) FMA + 1 MUL
+        }
+      return f;
+    }
+    case PK_DIAG_R: return q.diag_one0 ? 6 : 12;
+    default: return 12;  // ANTI, DIAG_T, DIAG_G: two complex multiplies per pair
+  }
+}
+
+double pass_flops(const TapeInfo& t, const StreamPlan& P, int pass) {
+  const PassDesc& pd = P.passes[pass];
+  double f = 0;
+  for (int g = pd.pgate_begin; g < pd.pgate_begin + pd.pgate_count; ++g) {
+    const PhaseGate& q = P.phase_gates[g];
+    const int ctrl = popc(q.cmR) + popc(q.cmT) + popc(q.gcm);
+    f += phase_gate_flops(q, t.mats[q.mat]) * std::ldexp(1.0, t.n - 1 - ctrl);
+  }
+  return f;
 }
 
 }  // namespace qsb

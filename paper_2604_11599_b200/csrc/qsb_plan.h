@@ -47,6 +47,16 @@ struct StreamPlan {
   int64_t descriptor_gates = 0;     // gates folded into decide regions
 };
 
+// Dense-matrix structure known before execution (literal matrices by value, ParamRef
+// angles by base): shared by the JIT code generator and the FLOP accounting.
+enum DenseVariant { DV_GEN, DV_REAL, DV_RX };
+DenseVariant dense_variant(const MatSrc& m);
+uint32_t zero_mask(const MatSrc& m);  // bit i: component m[i] is exactly zero
+// floating-point operations (FMA = 2) the specialised kernels spend per affected pair
+double phase_gate_flops(const PhaseGate& q, const MatSrc& m);
+// flops per state of one pass (sum over its gates and affected pairs)
+double pass_flops(const TapeInfo& t, const StreamPlan& P, int pass);
+
 // rb = register bits of k_pass_reg (4 for complex128, 5 for complex64); phases are
 // built when k - rb >= 5 (at least one warp per tile), else the shared-memory kernel runs.
 std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz_bits, StreamPlan& out);
