@@ -136,6 +136,14 @@ int32_t qsb_apply_gate(qsb_state st, const qsb_op* op, const double* params, int
 int32_t qsb_measure(qsb_state st, int32_t qubit, double u, int32_t* outcome, double* p1);
 /* reset (sim.py:254-259)                                                             */
 int32_t qsb_reset(qsb_state st, int32_t qubit, double u, int32_t* outcome);
+
+/* slice primitives of the global-qubit-sliced engine (sliced.py): the measurement of
+ * sim.py:230-251 split into a deterministic partial p1 (summed across slices in rank
+ * order by the host) and the collapse; a complex scale for diagonal gates and
+ * projections on global qubits.                                                       */
+int32_t qsb_state_prob1(qsb_state st, int32_t qubit, double* p1);  /* qubit < 0: sum of |a|^2 */
+int32_t qsb_state_collapse(qsb_state st, int32_t qubit, int32_t outcome, double scale, int32_t flip);
+int32_t qsb_state_scale(qsb_state st, double re, double im);
 /* expval_pauli (sim.py:420-430): xmask = X|Y letters, zmask = Z|Y letters, ny = #Y   */
 int32_t qsb_expval_pauli(qsb_state st, uint64_t xmask, uint64_t zmask, int32_t ny, double* out);
 

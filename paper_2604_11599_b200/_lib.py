@@ -109,6 +109,9 @@ _SIGS = {
     "qsb_plan_summary": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "qsb_jit_selftest": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _P]),
     "qsb_debug_fma_peak": (_I32, [_P, _I32, _PD]),
+    "qsb_state_prob1": (_I32, [_P, _I32, _PD]),
+    "qsb_state_collapse": (_I32, [_P, _I32, _I32, _D, _I32]),
+    "qsb_state_scale": (_I32, [_P, _D, _D]),
 }
 
 EXPORTED = tuple(_SIGS)

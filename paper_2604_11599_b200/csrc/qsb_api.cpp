@@ -620,6 +620,33 @@ int32_t qsb_measure(qsb_state st, int32_t qubit, double u, int32_t* outcome, dou
   return QSB_OK;
 }
 
+int32_t qsb_state_prob1(qsb_state st, int32_t qubit, double* p1) {
+  if (qubit >= st->n) return fail(QSB_ERR_ARG, "qubit out of range");
+  DeviceGuard g(st->ctx->device);
+  double* sc = st->scratch.as<double>();
+  launch_prob(st->c64, st->amps.p, st->n, qubit < 0 ? -1 : qubit, sc + 8, sc, st->ctx->stream);
+  QSB_CUDA(cudaMemcpyAsync(p1, sc, sizeof(double), cudaMemcpyDeviceToHost, st->ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  return QSB_OK;
+}
+
+int32_t qsb_state_collapse(qsb_state st, int32_t qubit, int32_t outcome, double scale, int32_t flip) {
+  if (qubit < 0 || qubit >= st->n) return fail(QSB_ERR_ARG, "qubit out of range");
+  DeviceGuard g(st->ctx->device);
+  launch_collapse(st->c64, st->amps.p, st->n, qubit, outcome ? 1 : 0, scale, flip ? 1 : 0, st->ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
+int32_t qsb_state_scale(qsb_state st, double re, double im) {
+  DeviceGuard g(st->ctx->device);
+  double m[8] = {re, im, 0, 0, 0, 0, re, im};  // diag(c, c) on qubit 0 == global scale
+  if (st->n == 0) return fail(QSB_ERR_ARG, "qsb_state_scale needs at least one qubit");
+  launch_apply_1q(st->c64, st->amps.p, st->n, 0, 0, 0, GC_DIAG, m, st->ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
 int32_t qsb_reset(qsb_state st, int32_t qubit, double u, int32_t* outcome) {
   if (qubit < 0 || qubit >= st->n) return fail(QSB_ERR_ARG, "qubit out of range");
   DeviceGuard g(st->ctx->device);
