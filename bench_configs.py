@@ -1,0 +1,131 @@
+"""Secondary benchmark: every BASELINE.json config on one B200 (bench.py carries the
+headline cfg 2 line of the driver contract).  One JSON line per config.
+
+  cfg1  IBM feedforward suite (FF1..FF6), <= 5 qubits, 1024 shots, complex128 -- resident engine
+  cfg2  DYN20 (see bench.py), reported here in complex64 as well
+  cfg3  VQE24: 24-qubit HEA, 8 layers, 200-term Hamiltonian, points batched -- observe()
+  cfg4  RDC30: 30-qubit random dynamic circuit, one trajectory, complex128 and complex64
+  cfg5  sliced execution (emulated on one GPU: 8 slices), RDC with 3 global qubits
+
+    python bench_configs.py [--only cfg1,cfg3] [--vqe-points 64] [--rdc-depth 200]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+
+def _emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def cfg1(args):
+    from paper_2604_11599_b200 import ir, sim, workloads
+
+    out = {}
+    for name, (_, k) in workloads.ff_suite().items():
+        b = ir.bind(k, [])
+        sim.sample(b, 1024, 1234)  # compile + warm
+        t0 = time.perf_counter()
+        reps = 20
+        for _ in range(reps):
+            h = sim.sample(b, 1024, 1234)
+        dt = (time.perf_counter() - t0) / reps
+        st = sim.last_stats()
+        out[name] = {"shots_per_s_e2e": 1024 / dt, "device_ms": st["total_ms"], "shots_per_s_device": 1024 / (st["total_ms"] / 1e3),
+                     "gate_updates": st["gate_updates"], "engine": "resident" if st["engine"] == 0 else "streaming"}
+    _emit({"config": "cfg1 IBM feedforward suite, 1024 shots, complex128", "results": out})
+
+
+def cfg2_c64(args):
+    from paper_2604_11599_b200 import ir, sim, workloads
+
+    _, k = workloads.dyn_circuit()
+    b = ir.bind(k, [])
+    B = args.batch
+    for prec in ("c128", "c64"):
+        sim.sample_words(b, B, 1234, precision=prec)
+        ms, shots = 0.0, 0
+        for s in range(2):
+            sim.sample_words(b, B, 1234, shot_begin=(s + 1) * B, precision=prec)
+            ms += sim.last_stats()["total_ms"]
+            shots += B
+        _emit({"config": f"cfg2 DYN20 {prec}", "shots_per_s": shots / (ms / 1e3), "batch": B})
+
+
+def cfg3(args):
+    import numpy as np
+
+    from paper_2604_11599_b200 import sim, workloads
+
+    _, k = workloads.vqe_ansatz()
+    ham = workloads.vqe_hamiltonian()
+    pts = workloads.vqe_points(args.vqe_points, k.total_params)
+    for prec in ("c128", "c64"):
+        sim.observe(k, ham, pts[:2], precision=prec)  # compile + warm
+        t0 = time.perf_counter()
+        e = sim.observe(k, ham, pts, precision=prec)
+        dt = time.perf_counter() - t0
+        st = sim.last_stats()
+        _emit({"config": f"cfg3 VQE24 200 terms {prec}", "points": len(pts), "points_per_s_e2e": len(pts) / dt,
+               "device_ms": st["total_ms"], "points_per_s_device": len(pts) / (st["total_ms"] / 1e3),
+               "gate_pass_ms": st["pass_ms"], "energy0": float(e[0]),
+               "extrapolated_4096_points_s": 4096 * dt / len(pts)})
+
+
+def cfg4(args):
+    from paper_2604_11599_b200 import ir, sim, workloads
+
+    _, k = workloads.rdc_circuit(n=30, depth=args.rdc_depth, every=20, seed=30200)
+    b = ir.bind(k, [])
+    for prec in ("c128", "c64"):
+        t0 = time.perf_counter()
+        words, tape = sim.sample_words(b, 1, 1234, precision=prec)
+        first = time.perf_counter() - t0
+        st = sim.last_stats()
+        t0 = time.perf_counter()
+        words, tape = sim.sample_words(b, 1, 1234, precision=prec)
+        dt = time.perf_counter() - t0
+        st = sim.last_stats()
+        _emit({"config": f"cfg4 RDC30 depth {args.rdc_depth} {prec}", "trajectory_s_e2e": dt,
+               "first_call_s_incl_jit": first, "device_ms": st["total_ms"], "passes": st["passes"],
+               "gate_updates": st["gate_updates"], "gate_updates_per_s": st["gate_updates"] / (st["total_ms"] / 1e3),
+               "hbm_gbs_pass": st["pass_bytes"] / (st["pass_ms"] / 1e3) / 1e9,
+               "fp_tflops_pass": st["pass_flops"] / (st["pass_ms"] / 1e3) / 1e12, "key": tape.keys(words)[0]})
+
+
+def cfg5(args):
+    from paper_2604_11599_b200 import ir, sim, sliced, workloads
+
+    n = args.sliced_qubits
+    _, k = workloads.rdc_circuit(n=n, depth=40, every=20, seed=34)
+    b = ir.bind(k, [])
+    t0 = time.perf_counter()
+    store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(1234, 0), 3)
+    dt = time.perf_counter() - t0
+    _emit({"config": f"cfg5 sliced RDC{n} depth 40, 3 global qubits emulated on 1 GPU (8 slices)",
+           "trajectory_s": dt, "exchanges": st.exchanges, "key": store.key()})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,cfg5")
+    ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--vqe-points", type=int, default=64)
+    ap.add_argument("--rdc-depth", type=int, default=200)
+    ap.add_argument("--sliced-qubits", type=int, default=26)
+    args = ap.parse_args()
+    table = {"cfg1": cfg1, "cfg2": cfg2_c64, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+    for name in args.only.split(","):
+        table[name](args)
+
+
+if __name__ == "__main__":
+    main()
