@@ -673,8 +673,92 @@ int32_t qsb_reset(qsb_state st, int32_t qubit, double u, int32_t* outcome) {
 // ---- Pauli expectation (shared by qsb_expval_pauli and qsb_observe) -----------------
 namespace {
 
+// Tile-fused reducer: group terms so that each group's X supports fit in one k-qubit
+// tile set (greedy first fit, larger supports first); Z-only terms join the first group.
+int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t slots, const uint64_t* xm,
+                       const uint64_t* zm, const int32_t* ny, int nterm, double* out_host) {
+  const int k = std::min(12, n), lowq = std::min(2, k);
+  const uint64_t lowmask = (1ull << lowq) - 1;
+  std::vector<int> order(nterm);
+  for (int t = 0; t < nterm; ++t) order[t] = t;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return __builtin_popcountll(xm[a]) > __builtin_popcountll(xm[b]);
+  });
+  struct Grp { uint64_t S; std::vector<int> terms; };
+  std::vector<Grp> groups;
+  std::vector<int> diag;
+  for (int t : order) {
+    if (xm[t] == 0) {
+      diag.push_back(t);
+      continue;
+    }
+    bool placed = false;
+    for (Grp& g : groups)
+      if (__builtin_popcountll(g.S | xm[t]) <= k) {
+        g.S |= xm[t];
+        g.terms.push_back(t);
+        placed = true;
+        break;
+      }
+    if (!placed) groups.push_back({lowmask | xm[t], {t}});
+  }
+  if (groups.empty()) groups.push_back({lowmask, {}});
+  for (int t : diag) groups[0].terms.push_back(t);
+  std::vector<ExpvalTerm> dev_terms, by_out(nterm);
+  std::vector<ExpvalGroup> dev_groups;
+  for (Grp& g : groups) {
+    for (int q = 0; q < n && __builtin_popcountll(g.S) < k; ++q) g.S |= 1ull << q;
+    ExpvalGroup eg{};
+    eg.smask = g.S;
+    eg.k = k;
+    eg.lowq = lowq;
+    eg.term_begin = (int)dev_terms.size();
+    eg.nterm = (int)g.terms.size();
+    auto compress = [&](uint64_t m) {
+      uint32_t out = 0;
+      int j = 0;
+      for (uint64_t s = g.S; s; s &= s - 1, ++j)
+        if (m & (s & (~s + 1))) out |= 1u << j;
+      return out;
+    };
+    for (int t : g.terms) {
+      ExpvalTerm e{};
+      e.xl = compress(xm[t]);
+      e.zl = compress(zm[t] & g.S);
+      e.xg = xm[t] & ~g.S;
+      e.zg = zm[t] & ~g.S;
+      e.ny = ny[t];
+      e.out = t;
+      dev_terms.push_back(e);
+      by_out[t] = e;
+    }
+    dev_groups.push_back(eg);
+  }
+  const int ntl = n - k;
+  const size_t pbytes = sizeof(double) * (size_t)slots * nterm * ((size_t)1 << ntl);
+  QSB_CUDA(ctx->misc.ensure(pbytes + 64));
+  QSB_CUDA(ctx->misc2.ensure(sizeof(ExpvalTerm) * 2 * (nterm + 1) + sizeof(double) * nterm * slots + 64));
+  char* base = ctx->misc2.as<char>();
+  ExpvalTerm* d_terms = reinterpret_cast<ExpvalTerm*>(base);
+  ExpvalTerm* d_byout = d_terms + (nterm + 1);
+  double* d_out = reinterpret_cast<double*>(d_byout + (nterm + 1));
+  if (nterm) {
+    QSB_CUDA(cudaMemcpyAsync(d_terms, dev_terms.data(), sizeof(ExpvalTerm) * nterm, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    QSB_CUDA(cudaMemcpyAsync(d_byout, by_out.data(), sizeof(ExpvalTerm) * nterm, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  for (const ExpvalGroup& g : dev_groups)
+    if (g.nterm) launch_expval_tile(c64, amps, n, slots, g, d_terms, ctx->misc.as<double>(), nterm, ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  launch_expval_tile_finish(ctx->misc.as<double>(), slots, nterm, ntl, d_byout, d_out, ctx->stream);
+  QSB_CUDA(cudaMemcpyAsync(out_host, d_out, sizeof(double) * nterm * slots, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return check_sticky();
+}
+
 int expval_terms(qsb_ctx ctx, int c64, const void* amps, int n, int64_t slots, const uint64_t* xm,
                  const uint64_t* zm, const int32_t* ny, int nterm, double* out_host /*[slots][nterm]*/) {
+  if (n >= 1 && nterm > 0) return expval_terms_tiled(ctx, c64, amps, n, slots, xm, zm, ny, nterm, out_host);
   std::map<uint64_t, std::vector<int>> groups;
   for (int t = 0; t < nterm; ++t) groups[xm[t]].push_back(t);
   int blocks = expval_blocks(n);

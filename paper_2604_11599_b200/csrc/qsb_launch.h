@@ -34,6 +34,22 @@ void launch_expval_group(int c64, const void* amps, int n, int64_t slots, const 
 void launch_expval_finish(const double* partial, int64_t slots, int nterm_total, int blocks,
                           const uint64_t* xmask, const int32_t* ny, double* out /*[slots][nterm]*/, cudaStream_t s);
 
+// tile-fused Pauli reducer (qsb_expval.cu)
+struct ExpvalTerm {
+  uint32_t xl, zl;  // X|Y and Z|Y letters inside the tile (tile positions)
+  uint64_t xg, zg;  // outside the tile (qubit masks; xg must be 0 for the tile path)
+  int32_t ny, out;  // #Y, output index
+};
+struct ExpvalGroup {
+  uint64_t smask;   // tile qubits
+  int32_t k, lowq, term_begin, nterm;
+};
+void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
+                        const ExpvalTerm* terms, double* partial /*[slots][nterm_total][tiles]*/, int nterm_total,
+                        cudaStream_t s);
+void launch_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
+                               const ExpvalTerm* terms_by_out, double* out, cudaStream_t s);
+
 // static sampling
 void launch_cumsum_seq(int c64, const void* amps, int n, double* cdf, cudaStream_t s);
 void launch_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
