@@ -73,9 +73,11 @@ struct qsb_ctx_s {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<cudaEvent_t> pass_events;
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
-  DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace;
+  int64_t opt_dedup = 1;
+  DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
   qsb_stats last{};
   double run_flops = 0;  // floating-point work of the pass kernels in the current run
+  bool run_physical = false;  // dedup ran: bytes / flops come from the device counters
 };
 
 struct qsb_state_s {
@@ -249,6 +251,7 @@ struct StreamRun {
   int max_trace;
   int32_t* ntrace;
   const uint64_t* rng_init = nullptr;
+  bool physical_counted = false;
   uint64_t final_clear = 0;
   int final_consumed = 0;
   double pass_bytes = 0;
@@ -262,6 +265,7 @@ int alloc_stream_scratch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, in
   QSB_CUDA(ctx->guards.ensure(sizeof(uint32_t) * t.gwords * slots));
   int64_t pstride = ((int64_t)1 << P.ntiles_log2) * P.max_local_bins;
   QSB_CUDA(ctx->partial.ensure(sizeof(double) * pstride * slots));
+  QSB_CUDA(ctx->dedup.ensure(sizeof(int32_t) * (3 * slots + 4)));
   return QSB_OK;
 }
 
@@ -296,8 +300,25 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   a.trace_out = r.trace;
   a.max_trace = r.max_trace;
   a.ntrace_out = r.ntrace;
-  launch_ctl_init(a.ctl, a.bits, t.nwords, a.guards, t.gwords, r.slots, r.seed, r.shot_begin, r.rng_init, ctx->stream);
+  // dedup is valid only when every slot runs the same circuit (shared matrices): it is
+  // off for observe(), whose slots are different parameter points
+  const bool dedup = ctx->opt_dedup && r.slots > 1 && r.mat_stride == 0;
+  int32_t* d_new_rep = ctx->dedup.as<int32_t>();
+  int32_t* d_copy_src = d_new_rep + r.slots;
+  int32_t* d_active = d_copy_src + r.slots;
+  int32_t* d_nactive = d_active + r.slots;
+  double* d_phys = reinterpret_cast<double*>(ctx->counters.as<char>() + 16);  // [bytes, flops] physical
+  launch_ctl_init(a.ctl, a.bits, t.nwords, a.guards, t.gwords, r.slots, r.seed, r.shot_begin, r.rng_init, dedup ? 1 : 0,
+                  ctx->stream);
   r.launches++;
+  if (dedup) {
+    a.active = d_active;
+    a.nactive = d_nactive;
+    launch_dedup(a, d_new_rep, d_copy_src, d_active, d_nactive, r.c64, false, ctx->stream);
+    r.launches += 2;
+  }
+  r.physical_counted = dedup;
+  if (dedup) ctx->run_physical = true;
   if (P.passes.empty()) {
     launch_init_zero(r.c64, r.state, t.n, r.slots, ctx->stream);
     r.launches++;
@@ -322,6 +343,11 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
       r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
       ctx->run_flops += r.pd->pflops[s.index] * (double)r.slots;
+      if (dedup) {  // the kernels touched only the representatives
+        launch_accum_physical(d_nactive, r.pd->pflops[s.index],
+                              (pd.init_zero ? 1.0 : 2.0) * state_bytes / (double)r.slots, d_phys, ctx->stream);
+        r.launches++;
+      }
       r.passes++;
       r.launches++;
       acc |= pd.smask;
@@ -331,6 +357,10 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
       QSB_CUDA(launch_decide(a, rd, ctx->stream));
       r.decides++;
       r.launches++;
+      if (dedup) {
+        launch_dedup(a, d_new_rep, d_copy_src, d_active, d_nactive, r.c64, true, ctx->stream);
+        r.launches += 4;
+      }
       acc = 0;
       consumed = 0;
     }
@@ -370,8 +400,14 @@ int64_t pick_batch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, int c64,
 
 int finish_stats(qsb_ctx ctx, float total_ms, double pass_ms, double pass_bytes, int64_t passes, int64_t decides,
                  int64_t launches, int engine, int k) {
-  unsigned long long cnt[2] = {0, 0};
+  unsigned long long cnt[4] = {0, 0, 0, 0};
   QSB_CUDA(cudaMemcpy(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+  if (ctx->run_physical) {  // history dedup: what the kernels actually moved / computed
+    double phys[2];
+    std::memcpy(phys, &cnt[2], sizeof(phys));
+    pass_bytes = phys[0];
+    ctx->run_flops = phys[1];
+  }
   ctx->last.kernel_launches = launches;
   ctx->last.passes = passes;
   ctx->last.decides = decides;
@@ -444,7 +480,8 @@ int32_t qsb_ctx_destroy(qsb_ctx ctx) {
   DeviceGuard g(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->state, &ctx->partial, &ctx->ctl, &ctx->bits, &ctx->guards, &ctx->mats, &ctx->params,
-                    &ctx->predrawn, &ctx->status, &ctx->counters, &ctx->misc, &ctx->misc2, &ctx->trace})
+                    &ctx->predrawn, &ctx->status, &ctx->counters, &ctx->misc, &ctx->misc2, &ctx->trace,
+                    &ctx->dedup})
     b->release();
   for (auto e : ctx->pass_events) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_a);
@@ -468,11 +505,12 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "engine") ctx->opt_engine = value;  // -1 auto, 0 resident, 1 streaming
   else if (k == "jit") ctx->opt_jit = value;        // NVRTC per-pass kernels (1) or generic kernel (0)
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
+  else if (k == "dedup") ctx->opt_dedup = value;    // branch-history deduplication of trajectories
   else if (k == "release_scratch") {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->state, &ctx->partial, &ctx->ctl, &ctx->bits, &ctx->guards, &ctx->mats, &ctx->params,
-                      &ctx->predrawn, &ctx->status, &ctx->misc, &ctx->misc2, &ctx->trace})
+                      &ctx->predrawn, &ctx->status, &ctx->misc, &ctx->misc2, &ctx->trace, &ctx->dedup})
       b->release();
   } else return fail(QSB_ERR_ARG, "unknown option " + k);
   return QSB_OK;
@@ -888,8 +926,9 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
   DeviceGuard g(ctx->device);
   const TapeInfo& t = tp->info;
   const int c64 = precision == QSB_C64 ? 1 : 0;
-  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 32, ctx->stream));
   ctx->run_flops = 0;
+  ctx->run_physical = false;
   RunTimer timer(ctx);
   const double* d_params = nullptr;
   int rc = upload_params(tp, params, 1, &d_params);
@@ -989,8 +1028,9 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
   const int c64 = precision == QSB_C64 ? 1 : 0;
   if (state_out && (state_out->n != t.n || state_out->c64 != c64))
     return fail(QSB_ERR_DIMENSION, "state_out shape / precision mismatch");
-  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 32, ctx->stream));
   ctx->run_flops = 0;
+  ctx->run_physical = false;
   RunTimer timer(ctx);
   const double* d_params = nullptr;
   int rc = upload_params(tp, params, 1, &d_params);
@@ -1102,8 +1142,9 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
   qsb_ctx ctx = tp->ctx;
   DeviceGuard g(ctx->device);
   const int c64 = out->c64;
-  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 32, ctx->stream));
   ctx->run_flops = 0;
+  ctx->run_physical = false;
   RunTimer timer(ctx);
   const double* d_params = nullptr;
   int rc = upload_params(tp, params, 1, &d_params);
@@ -1207,8 +1248,9 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   qsb_ctx ctx = tp->ctx;
   DeviceGuard g(ctx->device);
   const int c64 = precision == QSB_C64 ? 1 : 0;
-  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 16, ctx->stream));
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 32, ctx->stream));
   ctx->run_flops = 0;
+  ctx->run_physical = false;
   RunTimer timer(ctx);
   PlanDev* pd;
   int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);

@@ -168,6 +168,9 @@ struct TrajCtl {
   int32_t draws;         // uniforms consumed (pre-drawn streams)
   int32_t pad;
   int64_t gates;         // executed Gate ops (logical gate updates)
+  uint64_t hist;         // hash of the executed measure / reset outcomes so far
+  int32_t rep;           // slot whose state buffer holds this trajectory's state (history dedup)
+  int32_t pad2;
 };
 
 // kernel arguments of the streaming engine (passed by value)
@@ -198,6 +201,10 @@ struct StreamArgs {
   int64_t* trace_out;
   int32_t max_trace;
   int32_t* ntrace_out;
+  // branch-history deduplication: passes run only the representative slots listed in
+  // active[0 .. *nactive) (null: every slot)
+  const int32_t* active;
+  const int32_t* nactive;
 };
 
 QSB_HD uint64_t insert_zero(uint64_t v, int pos) {

@@ -89,7 +89,14 @@ cudaError_t launch_resident(const ResidentArgs& a, int num_sms, cudaStream_t s);
 void launch_mats_prep(const MatSrc* src, int nmat, const double* params, int nparams, int64_t slots,
                       double* mats_out, cudaStream_t s);
 void launch_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards, int gwords, int64_t slots,
-                     uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, cudaStream_t s);
+                     uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, int dedup, cudaStream_t s);
+// history dedup bookkeeping: regroup + copy (after a decide) or initial grouping, then
+// the representative list the passes iterate
+void launch_dedup(const StreamArgs& a, int32_t* new_rep, int32_t* copy_src, int32_t* active, int32_t* nactive,
+                  int c64, bool regroup, cudaStream_t s);
+// physical pass work under dedup: phys[0] += bytes_per_state * nactive, phys[1] += flops * nactive
+void launch_accum_physical(const int32_t* nactive, double flops_per_state, double bytes_per_state, double* phys,
+                           cudaStream_t s);
 
 cudaError_t launch_pass(const StreamArgs& a, const PassDesc& pd, cudaStream_t s);
 // register-blocked variant (qsb_pass_reg.cu), used when the pass has phases

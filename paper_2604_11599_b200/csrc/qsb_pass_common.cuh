@@ -54,7 +54,7 @@ struct PassItem {
 
 __device__ __forceinline__ PassItem pass_item(const StreamArgs& a, const PassDesc& pd, int64_t w, int ntl) {
   PassItem it;
-  it.slot = w >> ntl;
+  it.slot = a.active ? a.active[w >> ntl] : (w >> ntl);  // representative slots only (history dedup)
   const uint64_t tile = (uint64_t)w & ((1ull << ntl) - 1);
   const TrajCtl* c = a.ctl + it.slot;
   it.alive = c->status == 0;
@@ -129,7 +129,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   }
   __syncthreads();
   const int ntl = a.n - k;
-  const int64_t W = (int64_t)a.slots << ntl;
+  const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << ntl;
   const uint64_t qmask = (a.n >= 64) ? ~0ull : ((1ull << a.n) - 1);
 
   auto prefetch = [&](const PassItem& it, A* dst) {

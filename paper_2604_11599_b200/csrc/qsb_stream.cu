@@ -44,7 +44,7 @@ __global__ void k_mats_prep(const MatSrc* src, int nmat, const double* params, i
 }
 
 __global__ void k_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards, int gwords, int64_t slots,
-                           uint64_t seed, int64_t shot_begin, const uint64_t* rng_init) {
+                           uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, int dedup) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= slots) return;
   TrajCtl c;
@@ -65,6 +65,9 @@ __global__ void k_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* g
   c.draws = 0;
   c.pad = 0;
   c.gates = 0;
+  c.hist = 0;
+  c.rep = dedup ? 0 : (int32_t)s;  // identical (empty) histories share slot 0's state
+  c.pad2 = 0;
   ctl[s] = c;
   for (int w = 0; w < nwords; ++w) bits[s * nwords + w] = 0;
   for (int w = 0; w < gwords; ++w) guards[s * gwords + w] = 0;
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(kPT) k_pass(StreamArgs a, PassDesc pd) {
   const int tid = threadIdx.x;
   const int64_t slot = blockIdx.y;
   const TrajCtl* c = a.ctl + slot;
-  if (c->status) return;
+  if (c->status || c->rep != slot) return;  // dead, or its state lives in its representative
   const int n = a.n;
   const uint64_t qmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
   const uint64_t S = pd.smask;
@@ -239,7 +242,8 @@ __global__ void __launch_bounds__(kDT) k_decide(StreamArgs a, RegionDesc rd) {
   if (rd.has_marginal) {
     const int nbl = 1 << rd.m_local;
     const int ntl = a.ntiles_log2;
-    const double* part = a.partial + slot * a.partial_stride;
+    // the marginal of this trajectory's state was accumulated by its representative
+    const double* part = a.partial + (int64_t)cp->rep * a.partial_stride;
     uint64_t gm = 0;
     for (int j = 0; j < rd.mcount; ++j)
       if (rd.mtile_bit[j] >= 0) gm |= 1ull << rd.mtile_bit[j];
@@ -350,6 +354,10 @@ __global__ void __launch_bounds__(kDT) k_decide(StreamArgs a, RegionDesc rd) {
       break;
     }
     double s = 1.0 / sqrt(pout);
+    {  // history hash: equal histories <=> equal states (deduplication key)
+      uint64_t hx = c.hist + 0x9E3779B97F4A7C15ull * (uint64_t)(2 * op.op_index + outcome + 1);
+      c.hist = splitmix_next(hx);
+    }
     K |= 1ull << j;
     V = (V & ~(1ull << j)) | ((uint64_t)(outcome ^ (int)((Fp >> j) & 1)) << j);
     S.r *= s;
@@ -380,6 +388,55 @@ __global__ void __launch_bounds__(kDT) k_decide(StreamArgs a, RegionDesc rd) {
   c.depth = depth;
   c.active = active;
   *cp = c;
+}
+
+// ---- branch-history deduplication ------------------------
+// The state is a deterministic function of the executed outcome history, so slots with
+// equal histories share one state buffer.  After each decide: every slot's new
+// representative is the lowest alive slot with the same history hash; a slot that
+// becomes a representative while its state lived elsewhere copies the (pre-collapse)
+// buffer of its old representative, then applies its own collapse in the next pass.
+// The arithmetic per trajectory is unchanged, so results are bit-identical.
+__global__ void k_dedup_regroup(StreamArgs a, int32_t* new_rep, int32_t* copy_src) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= a.slots) return;
+  const TrajCtl c = a.ctl[s];
+  int32_t r = (int32_t)s;
+  if (c.status == 0) {
+    for (int64_t t = 0; t < s; ++t) {
+      const TrajCtl& o = a.ctl[t];
+      if (o.status == 0 && o.hist == c.hist) {
+        r = (int32_t)t;
+        break;
+      }
+    }
+  }
+  new_rep[s] = r;
+  copy_src[s] = (r == s && c.rep != s && c.status == 0) ? c.rep : -1;
+}
+
+__global__ void k_dedup_copy(StreamArgs a, const int32_t* copy_src, int64_t amp_bytes) {
+  const int64_t s = blockIdx.y;
+  const int32_t src = copy_src[s];
+  if (src < 0) return;
+  const int64_t words = (amp_bytes << a.n) / 16;
+  const int4* from = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(a.state) + (int64_t)src * (amp_bytes << a.n));
+  int4* to = reinterpret_cast<int4*>(reinterpret_cast<char*>(a.state) + s * (amp_bytes << a.n));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    to[i] = from[i];
+}
+
+__global__ void k_dedup_init_rep(StreamArgs a, int32_t* new_rep) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < a.slots) new_rep[s] = a.ctl[s].rep;
+}
+
+__global__ void k_dedup_commit(StreamArgs a, const int32_t* new_rep, int32_t* active, int32_t* nactive) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= a.slots) return;
+  const int32_t r = new_rep[s];
+  a.ctl[s].rep = r;
+  if (r == s && a.ctl[s].status == 0) active[atomicAdd(nactive, 1)] = (int32_t)s;  // order is irrelevant
 }
 
 __global__ void k_count(StreamArgs a, const int32_t* guard_gates, int nguards, int64_t unguarded,
@@ -422,9 +479,35 @@ void launch_mats_prep(const MatSrc* src, int nmat, const double* params, int npa
 }
 
 void launch_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards, int gwords, int64_t slots,
-                     uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, cudaStream_t s) {
+                     uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, int dedup, cudaStream_t s) {
   k_ctl_init<<<(unsigned)((slots + 127) / 128), 128, 0, s>>>(ctl, bits, nwords, guards, gwords, slots, seed,
-                                                            shot_begin, rng_init);
+                                                            shot_begin, rng_init, dedup);
+}
+
+__global__ void k_accum_physical(const int32_t* nactive, double flops, double bytes, double* phys) {
+  phys[0] += bytes * (double)*nactive;  // single thread: deterministic
+  phys[1] += flops * (double)*nactive;
+}
+
+void launch_accum_physical(const int32_t* nactive, double flops_per_state, double bytes_per_state, double* phys,
+                           cudaStream_t s) {
+  k_accum_physical<<<1, 1, 0, s>>>(nactive, flops_per_state, bytes_per_state, phys);
+}
+
+void launch_dedup(const StreamArgs& a, int32_t* new_rep, int32_t* copy_src, int32_t* active, int32_t* nactive,
+                  int c64, bool regroup, cudaStream_t s) {
+  const unsigned g = (unsigned)((a.slots + 127) / 128);
+  if (regroup) {
+    k_dedup_regroup<<<g, 128, 0, s>>>(a, new_rep, copy_src);
+    const int64_t amp = c64 ? 8 : 16;
+    const int64_t words = (amp << a.n) / 16;
+    unsigned chunks = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 2048), 64);
+    k_dedup_copy<<<dim3(chunks, (unsigned)a.slots), 256, 0, s>>>(a, copy_src, amp);
+  } else {  // initial grouping from ctl.rep
+    k_dedup_init_rep<<<g, 128, 0, s>>>(a, new_rep);
+  }
+  cudaMemsetAsync(nactive, 0, sizeof(int32_t), s);
+  k_dedup_commit<<<g, 128, 0, s>>>(a, new_rep, active, nactive);
 }
 
 static size_t pass_smem(int c64, const PassDesc& pd) {

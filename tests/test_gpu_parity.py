@@ -253,6 +253,24 @@ def test_jit_kernels_bit_identical_to_generic(prec):
         assert tape.keys(w1) == P.trajectory_keys(bd, 9, 0, 64)
 
 
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_history_dedup_bit_identical(prec):
+    """Trajectories with equal outcome histories share one state buffer; per-shot keys
+    (and therefore histograms) must not change, and the first segment of DYN-like
+    circuits must run on a single state (fewer physical bytes than logical)."""
+    _, k = workloads.dyn_circuit(n=14, layers=10, every=5, nmeas=3, seed=31)
+    b = ir.bind(k, [])
+    with option("dedup", 0, 1):
+        w0, tape = sim.sample_words(b, 300, 5, precision=prec)
+        logical = sim.last_stats()["pass_bytes"]
+    w1, _ = sim.sample_words(b, 300, 5, precision=prec)
+    physical = sim.last_stats()["pass_bytes"]
+    np.testing.assert_array_equal(w0, w1)
+    assert physical < logical
+    if prec == "c128":
+        assert tape.keys(w1[:40]) == P.trajectory_keys(b, 5, 0, 40)
+
+
 def test_per_op_api_matches_reference_semantics():
     from paper_2604_11599_b200.ir import Gate
 
