@@ -202,7 +202,10 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
     const bool need_skip = q.guard >= 0 || q.gcm != 0 || q.kind == PK_DIAG_G;
     o << "  {  // gate " << gi << " kind " << q.kind << "\n";
     if (need_skip) o << "  if (sg[" << gi << "].kind != " << (int)PK_SKIP << ") {\n";
-    o << "  const R* m = sg[" << gi << "].m;\n";
+    // literal matrices live in the module's constant bank (FMA operands straight from the
+    // constant cache, no registers / shared loads); ParamRef and per-CTA factors use staging
+    if (ms.has_matrix && q.kind != PK_DIAG_G) o << "  const R* m = qsb_cm + " << 8 * gi << ";\n";
+    else o << "  const R* m = sg[" << gi << "].m;\n";
     const bool thr = q.cmT != 0;
     if (thr) o << "  const bool c = (base & " << q.cmT << "u) == " << q.cvT << "u;\n";
     auto sel_pair = [&](int j0, int j1, const char* fn) {
@@ -297,11 +300,27 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
       o << sparse_helper(z);
     }
   }
+  {  // literal matrices of the pass, indexed by pass-relative gate (exact hex literals)
+    o << "__constant__ R qsb_cm[" << 8 * std::max(1, pd.pgate_count) << "] = {";
+    for (int g = 0; g < pd.pgate_count; ++g) {
+      const MatSrc& ms = t.mats[P.phase_gates[pd.pgate_begin + g].mat];
+      for (int i = 0; i < 8; ++i) {
+        char buf[64];
+        if (c64) snprintf(buf, sizeof(buf), "%af", (double)(float)ms.mat[i]);
+        else snprintf(buf, sizeof(buf), "%a", ms.mat[i]);
+        o << (g || i ? ", " : "") << buf;
+      }
+    }
+    if (!pd.pgate_count) o << "0";
+    o << "};\n";
+  }
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb);
   }
-  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
+  const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
+  o << "extern \"C\" __global__ void __launch_bounds__(256, " << (mb && *mb ? atoi(mb) : 2)
+    << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
   o << "  qsb::pass_persistent<R, 4>(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
   for (int i = 0; i < pd.phase_count; ++i) {
