@@ -254,9 +254,11 @@ def run_ours(args) -> None:
         prof = os.path.join(REPO, "profiles", "pass_kernel_traffic.json")
         if os.path.exists(prof):
             try:
-                # ncu dram bytes per state-pass x the states one pass launch processes here
-                per_state = json.load(open(prof)).get("traffic_bytes_per_state_pass")
-                traffic = per_state * B if (per_state and prec == "c128") else None
+                # ncu dram bytes / algorithmic bytes per state-pass, applied to this run's
+                # algorithmic bytes per pass launch (physical: dedup'd states excluded)
+                prof_d = json.load(open(prof))
+                ratio = prof_d["traffic_bytes_per_state_pass"] / prof_d["algorithmic_bytes_per_state_pass"]
+                traffic = ratio * pass_bytes / passes if (passes and prec == "c128") else None
             except Exception:
                 traffic = None
         line = {

@@ -107,7 +107,7 @@ _SIGS = {
     "qsb_observe": (_I32, [_P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P, _P]),
     "qsb_debug_rng": (_I32, [_P, _U64, _I64, _I32, _P]),
     "qsb_plan_summary": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
-    "qsb_jit_selftest": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _P]),
+    "qsb_jit_selftest": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "qsb_debug_fma_peak": (_I32, [_P, _I32, _PD]),
     "qsb_state_prob1": (_I32, [_P, _I32, _PD]),
     "qsb_state_collapse": (_I32, [_P, _I32, _I32, _D, _I32]),
@@ -175,6 +175,10 @@ class Context:
         self.handle = h
         self.device = device
         self.lib = lib
+        # QSB_OPTIONS="reg_bits=3,dedup=0": engine tuning knobs for experiments
+        for kv in filter(None, os.environ.get("QSB_OPTIONS", "").split(",")):
+            key, _, val = kv.partition("=")
+            self.set_option(key.strip(), int(val))
 
     def set_option(self, key: str, value: int) -> None:
         check(self.lib.qsb_ctx_set_option(self.handle, key.encode(), int(value)))

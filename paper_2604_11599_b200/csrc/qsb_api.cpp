@@ -73,7 +73,7 @@ struct qsb_ctx_s {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<cudaEvent_t> pass_events;
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
-  int64_t opt_dedup = 1;
+  int64_t opt_dedup = 1, opt_reg_bits = 4;
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
   qsb_stats last{};
   double run_flops = 0;  // floating-point work of the pass kernels in the current run
@@ -136,7 +136,7 @@ int upload_tape_device(qsb_tape tp) {
   return QSB_OK;
 }
 
-int reg_bits(int c64) { return 4; }
+int reg_bits(qsb_ctx ctx) { return (int)ctx->opt_reg_bits; }  // amplitudes per thread = 2^reg_bits
 
 int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
   const int c64 = lowq == 5 ? 1 : 0;
@@ -506,6 +506,10 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit") ctx->opt_jit = value;        // NVRTC per-pass kernels (1) or generic kernel (0)
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;    // branch-history deduplication of trajectories
+  else if (k == "reg_bits") {                       // register-blocked phases: 3 or 4 register qubits
+    if (value != 3 && value != 4) return fail(QSB_ERR_ARG, "reg_bits must be 3 or 4");
+    ctx->opt_reg_bits = value;
+  }
   else if (k == "release_scratch") {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
@@ -977,7 +981,7 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
+    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
     if (rc) return rc;
     int64_t B = pick_batch(ctx, t, pd->plan, c64, shot_count);
     QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
@@ -1093,7 +1097,7 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
+    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
     if (rc) return rc;
     QSB_CUDA(ctx->state.ensure(amp_bytes(c64) << t.n));
     StreamRun r{tp, pd, c64, 1, ctx->state.p, mats, mstride, seed, shot, d_pre, npredrawn, 0, d_trace, max_trace,
@@ -1176,7 +1180,7 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
     return QSB_OK;
   }
   PlanDev* pd;
-  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
+  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   StreamRun r{tp, pd, c64, 1, out->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
   rc = run_stream(ctx, r);
@@ -1253,7 +1257,7 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   ctx->run_physical = false;
   RunTimer timer(ctx);
   PlanDev* pd;
-  int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(c64), &pd);
+  int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   int64_t B = pick_batch(ctx, t, pd->plan, c64, npoints);
   QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
@@ -1355,13 +1359,14 @@ extern "C" int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqu
 }
 
 extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits,
-                                    int32_t nparams, int32_t precision, double* out) {
+                                    int32_t nparams, int32_t precision, int32_t reg_bits, double* out) {
   const int c64 = precision == QSB_C64 ? 1 : 0;
+  if (reg_bits != 3 && reg_bits != 4) return fail(QSB_ERR_ARG, "reg_bits must be 3 or 4");
   TapeInfo t;
   std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   StreamPlan P;
-  e = build_stream_plan(t, 12, c64 ? 5 : 4, 4, swizzle_bits(c64), P);
+  e = build_stream_plan(t, 12, c64 ? 5 : 4, reg_bits, swizzle_bits(c64), P);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   int nk = 0;
   double ms = 0;

@@ -139,7 +139,7 @@ struct PassDesc {
   int32_t m_local;      // |M ∩ S|
   int32_t mloc[kMaxMeasureRegion];   // local positions of M∩S, in M order
   int32_t region;       // decide region fed by the epilogue
-  int32_t pad;
+  int32_t rb;           // register bits of the phases (0: no phases, shared-memory kernel)
 };
 
 struct RegionDesc {

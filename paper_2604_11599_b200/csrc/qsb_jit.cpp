@@ -187,13 +187,14 @@ std::string sparse_helper(uint32_t z) {
 
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
                 const PhaseDesc& ph, int sb) {
+  const int nr = 1 << P.rb;  // amplitudes per thread
   o << "__device__ __noinline__ void ph" << ph_index
     << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
        "const int tid) {\n";
   o << "  const uint32_t base = 0u";
   for (int i = 0; i < ph.nt; ++i) o << " | ((((uint32_t)tid >> " << i << ") & 1u) << " << (int)ph.tpos[i] << ")";
   o << ";\n  const uint32_t sb = base ^ swz[base >> " << sb << "];\n";
-  for (int j = 0; j < 16; ++j) o << "  A v" << j << " = tile[sb ^ " << ph.soff[j] << "u];\n";
+  for (int j = 0; j < nr; ++j) o << "  A v" << j << " = tile[sb ^ " << ph.soff[j] << "u];\n";
   for (int gl = 0; gl < ph.gate_count; ++gl) {
     const int gidx = ph.gate_begin + gl;
     const PhaseGate& q = P.phase_gates[gidx];
@@ -239,7 +240,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
         } else if (q.kind == PK_DIAG_R) {
           fn = "G_DIAG";
         }
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < nr; ++j) {
           if (j & b) continue;
           if (((uint32_t)j & q.cmR) != q.cvR) continue;
           const int j1 = j | b;
@@ -258,11 +259,11 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
       case PK_DIAG_T: {
         o << "  const bool bt = (base >> " << q.tp << ") & 1u;\n";
         o << "  const R dr = bt ? m[6] : m[0], di = bt ? m[7] : m[1];\n";
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < nr; ++j)
           if (((uint32_t)j & q.cmR) == q.cvR) scale(j, "dr", "di");
       } break;
       case PK_DIAG_G: {
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < nr; ++j)
           if (((uint32_t)j & q.cmR) == q.cvR) scale(j, "m[0]", "m[1]");
       } break;
       default:
@@ -272,7 +273,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
     if (need_skip) o << "  }\n";
     o << "  }\n";
   }
-  for (int j = 0; j < 16; ++j) o << "  tile[sb ^ " << ph.soff[j] << "u] = v" << j << ";\n";
+  for (int j = 0; j < nr; ++j) o << "  tile[sb ^ " << ph.soff[j] << "u] = v" << j << ";\n";
   o << "}\n";
 }
 
@@ -319,10 +320,10 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
     if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb);
   }
   const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
-  o << "extern \"C\" __global__ void __launch_bounds__(256, " << (mb && *mb ? atoi(mb) : 2)
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pd.k - P.rb)) << ", " << (mb && *mb ? atoi(mb) : 2)
     << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-  o << "  qsb::pass_persistent<R, 4>(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
+  o << "  qsb::pass_persistent<R, " << P.rb << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) o << "    ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";
@@ -406,14 +407,15 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vect
     JitKernel& jk = out[j.pass];
     jk.lib = (void*)lib;
     jk.kern = (void*)k;
-    jk.smem = pass_reg_smem(c64, P.passes[j.pass], 4);
+    jk.smem = pass_reg_smem(c64, P.passes[j.pass], P.rb);
+    jk.threads = 1 << (P.passes[j.pass].k - P.rb);
     e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
     if (e != cudaSuccess) {
       jit_release(out);
       return std::string("cudaFuncSetAttribute (jit): ") + cudaGetErrorString(e);
     }
     int per_sm = 1, dev = 0, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, 1 << (P.passes[j.pass].k - 4), jk.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, jk.threads, jk.smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     jk.max_grid = (int64_t)std::max(1, per_sm) * sms;
@@ -449,7 +451,7 @@ cudaError_t jit_launch(const JitKernel& jk, const StreamArgs& a, const PassDesc&
   void* args[] = {(void*)&aa, (void*)&pp};
   const int64_t W = (int64_t)a.slots << (a.n - pd.k);
   dim3 grid((unsigned)std::min<int64_t>(W, jk.max_grid));
-  dim3 block((unsigned)(1u << (pd.k - 4)));
+  dim3 block((unsigned)jk.threads);
   return cudaLaunchKernel((const void*)jk.kern, grid, block, args, jk.smem, s);
 }
 

@@ -15,6 +15,7 @@ struct JitKernel {
   void* kern = nullptr;  // cudaKernel_t
   size_t smem = 0;
   int64_t max_grid = 148;  // resident CTAs (persistent kernel)
+  int threads = 256;       // 2^(k - register bits)
 };
 
 // true if libnvrtc could be loaded

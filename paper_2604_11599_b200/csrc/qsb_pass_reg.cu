@@ -60,7 +60,9 @@ __device__ __forceinline__ void ph_jt(int jt, typename Amp<R>::T* v, const R* m,
     case 0: ph_pair<R, NR, 0, KIND, CTRL>(v, m, cmR, cvR); break;
     case 1: ph_pair<R, NR, 1, KIND, CTRL>(v, m, cmR, cvR); break;
     case 2: ph_pair<R, NR, 2, KIND, CTRL>(v, m, cmR, cvR); break;
-    default: ph_pair<R, NR, 3, KIND, CTRL>(v, m, cmR, cvR); break;
+    default:
+      if constexpr (NR > 8) ph_pair<R, NR, 3, KIND, CTRL>(v, m, cmR, cvR);
+      break;
   }
 }
 
@@ -77,10 +79,9 @@ __device__ __forceinline__ void ph_scale(typename Amp<R>::T* v, R dr, R di, uint
     if (!CTRL || (((uint32_t)j & cmR) == cvR)) v[j] = cmul<R>(dr, di, v[j]);
 }
 
-template <typename R>
-__global__ void __launch_bounds__(256, 2) k_pass_reg(StreamArgs a, PassDesc pd) {
+template <typename R, int RB>
+__global__ void __launch_bounds__((1 << (12 - RB)), 2) k_pass_reg(StreamArgs a, PassDesc pd) {
   using A = typename Amp<R>::T;
-  constexpr int RB = 4;
   constexpr int NR = 1 << RB;
   constexpr int SB = sizeof(R) == 8 ? 3 : 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -149,24 +150,25 @@ int num_sms() {
   return sms;
 }
 
-template <typename R> cudaError_t launch_t(const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
-  const int T = 1 << (pd.k - 4);
-  const size_t sm = pass_reg_smem(a.c64, pd, 4);
-  cudaError_t e = cudaFuncSetAttribute(k_pass_reg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+template <typename R, int RB> cudaError_t launch_t(const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
+  const int T = 1 << (pd.k - RB);
+  const size_t sm = pass_reg_smem(a.c64, pd, RB);
+  cudaError_t e = cudaFuncSetAttribute(k_pass_reg<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_reg<R>, T, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_reg<R, RB>, T, sm);
   if (per_sm < 1) per_sm = 1;
   const int64_t W = (int64_t)a.slots << (a.n - pd.k);
   const int64_t grid = std::min<int64_t>(W, (int64_t)per_sm * num_sms());
-  k_pass_reg<R><<<(unsigned)grid, T, sm, s>>>(a, pd);
+  k_pass_reg<R, RB><<<(unsigned)grid, T, sm, s>>>(a, pd);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_pass_reg(const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
-  return a.c64 ? launch_t<float>(a, pd, s) : launch_t<double>(a, pd, s);
+  if (pd.rb == 3) return a.c64 ? launch_t<float, 3>(a, pd, s) : launch_t<double, 3>(a, pd, s);
+  return a.c64 ? launch_t<float, 4>(a, pd, s) : launch_t<double, 4>(a, pd, s);
 }
 
 }  // namespace qsb

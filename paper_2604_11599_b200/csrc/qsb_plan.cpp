@@ -394,7 +394,11 @@ struct Planner {
     pd.region = epi_region;
     pd.epi = epi_region >= 0 ? 1 : 0;
     pd.phase_begin = pd.phase_count = 0;
-    if (rb > 0 && pd.k - rb >= 5 && pd.k == k) build_phases(pd);
+    pd.rb = 0;
+    if (rb > 0 && pd.k - rb >= 5 && pd.k == k) {
+      build_phases(pd);
+      pd.rb = rb;
+    }
     P.passes.push_back(pd);
     P.steps.push_back({0, (int)P.passes.size() - 1});
   }
@@ -602,7 +606,8 @@ std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int sw
   lowq = std::max(0, std::min(lowq, k));
   out.k = k;
   out.lowq = lowq;
-  out.rb = (rb > 0 && k - rb >= 5) ? rb : 0;
+  // register-blocked kernels run 2^(k - rb) threads: one warp at least, 512 at most
+  out.rb = (rb > 0 && k - rb >= 5 && k - rb <= 9) ? rb : 0;
   out.ntiles_log2 = t.n - k;
   Planner pl(t, k, lowq, out.rb, out);
   pl.swz_bits_ = swz;

@@ -519,7 +519,7 @@ cudaError_t launch_pass(const StreamArgs& a, const PassDesc& pd, cudaStream_t s)
   size_t smem = pass_smem(a.c64, pd);
   dim3 grid((unsigned)(1ull << (a.n - pd.k)), (unsigned)a.slots);
   cudaError_t e;
-  if (a.phases && (pd.phase_count > 0 || pd.gate_count == 0) && pd.k - 4 >= 5)
+  if (a.phases && pd.rb > 0)
     return launch_pass_reg(a, pd, s);
   if (a.c64) {
     e = cudaFuncSetAttribute(k_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -347,6 +347,29 @@ def _flatten(ops, out: list, offsets: dict) -> None:
             out.append(("endif",))
 
 
+def tape_records(kernel) -> np.ndarray:
+    """The flat qsb_op record array of `kernel` (host only, no device needed)."""
+    offsets = _classical_offsets([(n, int(w)) for n, w in kernel.classical_layout])
+    flat: list = []
+    _flatten(kernel.body, flat, offsets)
+    recs = np.zeros(len(flat), dtype=_lib.OP_DTYPE)
+    for i, item in enumerate(flat):
+        r = recs[i]
+        if item[0] == "gate":
+            _gate_record(r, item[1], True)
+        elif item[0] == "measure":
+            r["kind"], r["qubit"], r["bit"] = _lib.OP_MEASURE, item[1], item[2]
+        elif item[0] == "reset":
+            r["kind"], r["qubit"] = _lib.OP_RESET, item[1]
+        elif item[0] == "if":
+            _pred_record(r, item[1], offsets)
+        elif item[0] == "else":
+            r["kind"] = _lib.OP_ELSE
+        else:
+            r["kind"] = _lib.OP_ENDIF
+    return recs
+
+
 class Tape:
     """A compiled Kernel on one device context (qsb_tape)."""
 
@@ -359,25 +382,9 @@ class Tape:
         self.nbits = sum(w for _, w in self.layout)
         self.nwords = max(1, (self.nbits + 63) // 64)
         self.nparams = sum(p.count for p in kernel.param_layout)
-        flat: list = []
-        _flatten(kernel.body, flat, self.offsets)
-        recs = np.zeros(len(flat), dtype=_lib.OP_DTYPE)
-        for i, item in enumerate(flat):
-            r = recs[i]
-            if item[0] == "gate":
-                _gate_record(r, item[1], True)
-            elif item[0] == "measure":
-                r["kind"], r["qubit"], r["bit"] = _lib.OP_MEASURE, item[1], item[2]
-            elif item[0] == "reset":
-                r["kind"], r["qubit"] = _lib.OP_RESET, item[1]
-            elif item[0] == "if":
-                _pred_record(r, item[1], self.offsets)
-            elif item[0] == "else":
-                r["kind"] = _lib.OP_ELSE
-            else:
-                r["kind"] = _lib.OP_ENDIF
+        recs = tape_records(kernel)
         self.records = recs
-        self.ngates_static = sum(1 for it in flat if it[0] == "gate")
+        self.ngates_static = int(np.count_nonzero(recs["kind"] == _lib.OP_GATE))
         h = ctypes.c_void_p()
         _lib.check(ctx.lib.qsb_tape_create(ctx.handle, _lib.ptr(recs), len(recs), self.n, self.nbits,
                                            self.nparams, ctypes.byref(h)))

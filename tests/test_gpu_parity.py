@@ -254,6 +254,27 @@ def test_jit_kernels_bit_identical_to_generic(prec):
 
 
 @pytest.mark.parametrize("prec", ["c128", "c64"])
+@pytest.mark.parametrize("jit", [0, 1])
+def test_register_blocking(prec, jit):
+    """8 or 16 amplitudes per thread regroup the gates into different phases, which
+    reorders commuting gates on disjoint qubits (a last-ulp effect, like any
+    reordering of (A x I)(I x B)): both blockings must match the oracle within the
+    precision's tolerance, and c128 trajectories must stay bit-exact."""
+    k = workloads.random_static(15, 300, seed=5, nparams=2, max_controls=2)
+    b = ir.bind(k, [0.4, -0.9])
+    _, kd = workloads.dyn_circuit(n=15, layers=10, every=5, nmeas=3, seed=23)
+    bd = ir.bind(kd, [])
+    want = P.final_state(b).amps
+    with option("jit", jit, 1):
+        for rb in (4, 3):
+            with option("reg_bits", rb, 4):
+                assert_state(sim.statevector(b, precision=prec).amps, want, TOL[prec])
+                words, tape = sim.sample_words(bd, 48, 3, precision=prec)
+                if prec == "c128":
+                    assert tape.keys(words) == P.trajectory_keys(bd, 3, 0, 48), rb
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
 def test_history_dedup_bit_identical(prec):
     """Trajectories with equal outcome histories share one state buffer; per-shot keys
     (and therefore histograms) must not change, and the first segment of DYN-like

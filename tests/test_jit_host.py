@@ -1,0 +1,43 @@
+"""Host-only check of the NVRTC pass-kernel generator (qsb_jit.cpp): every
+register-blocked pass of the benchmark tapes compiles for sm_100a at both register
+blockings (8 or 16 amplitudes per thread) and both precisions.  NVRTC runs without a
+device, so this guards the generated CUDA on the CPU box; execution parity is in
+test_gpu_parity.py."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2604_11599_b200 import _lib, sim, workloads
+
+
+def _selftest(kernel, precision, reg_bits):
+    lib = _lib.load()
+    recs = sim.tape_records(kernel)
+    nbits = sum(int(w) for _, w in kernel.classical_layout)
+    nparams = sum(p.count for p in kernel.param_layout)
+    out = np.zeros(2, dtype=np.float64)
+    rc = lib.qsb_jit_selftest(_lib.ptr(recs), len(recs), int(kernel.qubit_count), nbits, nparams, precision,
+                              reg_bits, _lib.ptr(out))
+    if rc != _lib.OK and b"nvrtc" in (lib.qsb_last_error() or b"").lower() and b"load" in lib.qsb_last_error():
+        pytest.skip("libnvrtc not loadable here")
+    _lib.check(rc)
+    return int(out[0])
+
+
+@pytest.mark.parametrize("reg_bits", [3, 4])
+@pytest.mark.parametrize("precision", [_lib.C128, _lib.C64])
+def test_dyn_passes_compile(precision, reg_bits):
+    _, k = workloads.dyn_circuit(n=14, layers=12, every=4, nmeas=3, seed=3)
+    assert _selftest(k, precision, reg_bits) > 0
+
+
+def test_reg_bits_rejected():
+    _, k = workloads.dyn_circuit(n=14, layers=4, every=4, nmeas=2, seed=1)
+    with pytest.raises(_lib.BackendError):
+        _selftest(k, _lib.C128, 5)
+
+
+def test_ctypes_signature():
+    assert _lib._SIGS["qsb_jit_selftest"][1][6] is ctypes.c_int32
