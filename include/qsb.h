@@ -201,7 +201,7 @@ int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqubits, int32
 
 /* host-only: generate and NVRTC-compile (no device needed, nothing loaded) the
  * specialised pass kernels of a tape's streaming plan; returns QSB_OK or QSB_ERR_ARG
- * with the compiler log in qsb_last_error().  reg_bits = 3 or 4 amplitude-register
+ * with the compiler log in qsb_last_error().  reg_bits = 3, 4 or 5 amplitude-register
  * qubits per thread.  out[0] = kernels, out[1] = milliseconds. */
 int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
                          int32_t precision, int32_t reg_bits, double* out);

@@ -506,8 +506,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit") ctx->opt_jit = value;        // NVRTC per-pass kernels (1) or generic kernel (0)
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;    // branch-history deduplication of trajectories
-  else if (k == "reg_bits") {                       // register-blocked phases: 3 or 4 register qubits
-    if (value != 3 && value != 4) return fail(QSB_ERR_ARG, "reg_bits must be 3 or 4");
+  else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
+    if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
     ctx->opt_reg_bits = value;
   }
   else if (k == "release_scratch") {
@@ -1361,7 +1361,7 @@ extern "C" int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqu
 extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits,
                                     int32_t nparams, int32_t precision, int32_t reg_bits, double* out) {
   const int c64 = precision == QSB_C64 ? 1 : 0;
-  if (reg_bits != 3 && reg_bits != 4) return fail(QSB_ERR_ARG, "reg_bits must be 3 or 4");
+  if (reg_bits < 3 || reg_bits > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
   TapeInfo t;
   std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);

@@ -60,8 +60,11 @@ __device__ __forceinline__ void ph_jt(int jt, typename Amp<R>::T* v, const R* m,
     case 0: ph_pair<R, NR, 0, KIND, CTRL>(v, m, cmR, cvR); break;
     case 1: ph_pair<R, NR, 1, KIND, CTRL>(v, m, cmR, cvR); break;
     case 2: ph_pair<R, NR, 2, KIND, CTRL>(v, m, cmR, cvR); break;
-    default:
+    case 3:
       if constexpr (NR > 8) ph_pair<R, NR, 3, KIND, CTRL>(v, m, cmR, cvR);
+      break;
+    default:
+      if constexpr (NR > 16) ph_pair<R, NR, 4, KIND, CTRL>(v, m, cmR, cvR);
       break;
   }
 }
@@ -168,6 +171,7 @@ template <typename R, int RB> cudaError_t launch_t(const StreamArgs& a, const Pa
 
 cudaError_t launch_pass_reg(const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
   if (pd.rb == 3) return a.c64 ? launch_t<float, 3>(a, pd, s) : launch_t<double, 3>(a, pd, s);
+  if (pd.rb == 5) return a.c64 ? launch_t<float, 5>(a, pd, s) : launch_t<double, 5>(a, pd, s);
   return a.c64 ? launch_t<float, 4>(a, pd, s) : launch_t<double, 4>(a, pd, s);
 }
 

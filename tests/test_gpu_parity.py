@@ -256,7 +256,7 @@ def test_jit_kernels_bit_identical_to_generic(prec):
 @pytest.mark.parametrize("prec", ["c128", "c64"])
 @pytest.mark.parametrize("jit", [0, 1])
 def test_register_blocking(prec, jit):
-    """8 or 16 amplitudes per thread regroup the gates into different phases, which
+    """8, 16 or 32 amplitudes per thread regroup the gates into different phases, which
     reorders commuting gates on disjoint qubits (a last-ulp effect, like any
     reordering of (A x I)(I x B)): both blockings must match the oracle within the
     precision's tolerance, and c128 trajectories must stay bit-exact."""
@@ -266,7 +266,7 @@ def test_register_blocking(prec, jit):
     bd = ir.bind(kd, [])
     want = P.final_state(b).amps
     with option("jit", jit, 1):
-        for rb in (4, 3):
+        for rb in (4, 3, 5):
             with option("reg_bits", rb, 4):
                 assert_state(sim.statevector(b, precision=prec).amps, want, TOL[prec])
                 words, tape = sim.sample_words(bd, 48, 3, precision=prec)

@@ -26,7 +26,7 @@ def _selftest(kernel, precision, reg_bits):
     return int(out[0])
 
 
-@pytest.mark.parametrize("reg_bits", [3, 4])
+@pytest.mark.parametrize("reg_bits", [3, 4, 5])
 @pytest.mark.parametrize("precision", [_lib.C128, _lib.C64])
 def test_dyn_passes_compile(precision, reg_bits):
     _, k = workloads.dyn_circuit(n=14, layers=12, every=4, nmeas=3, seed=3)
@@ -36,7 +36,7 @@ def test_dyn_passes_compile(precision, reg_bits):
 def test_reg_bits_rejected():
     _, k = workloads.dyn_circuit(n=14, layers=4, every=4, nmeas=2, seed=1)
     with pytest.raises(_lib.BackendError):
-        _selftest(k, _lib.C128, 5)
+        _selftest(k, _lib.C128, 6)
 
 
 def test_ctypes_signature():
