@@ -193,7 +193,6 @@ def run_ours(args) -> None:
     prec = args.precision
     tape = sim.compile_tape(kernel, local)  # compile once (excluded from timing, like lower())
     h2d_bytes = 8  # the step's seed / shot offset; DYN20 has no parameters
-    d2h_bytes = B * tape.nwords * 8 + B * 4
 
     def step_shots(step):  # disjoint global shot ranges per (step, rank)
         return (step * world + rank) * B
@@ -236,6 +235,9 @@ def run_ours(args) -> None:
         hists.append(sim.sample(bound, B, SEED, precision=prec, device=local))
     torch.cuda.synchronize(local)
     e2e_s = time.perf_counter() - t0
+    # sim.sample histograms on the device: per-shot status words + the distinct outcomes
+    # (8-byte word + 4-byte count each) + the distinct count come back
+    d2h_bytes = B * 4 + 4 + 12 * len(hists[-1].counts)
 
     t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
     g = torch.tensor([gate_updates, ties, launches], dtype=torch.float64, device=f"cuda:{local}")

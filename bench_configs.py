@@ -69,7 +69,7 @@ def cfg3(args):
     ham = workloads.vqe_hamiltonian()
     pts = workloads.vqe_points(args.vqe_points, k.total_params)
     for prec in ("c128", "c64"):
-        sim.observe(k, ham, pts[:2], precision=prec)  # compile + warm
+        sim.observe(k, ham, pts, precision=prec)  # compile + warm (buffers sized for the batch)
         t0 = time.perf_counter()
         e = sim.observe(k, ham, pts, precision=prec)
         dt = time.perf_counter() - t0

@@ -185,6 +185,18 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out);
 int32_t qsb_sample_static(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
                           int64_t shot_begin, int64_t shot_count, uint64_t* bits_out);
 
+/* sample (sim.py:372-391) with the shot histogram built on the device
+ * (ShotHistogram.counts, sim.py:122-131): the per-shot words of shots
+ * [shot_begin, shot_begin + shot_count) -- trajectory or static path, exactly as
+ * qsb_sample_trajectories / qsb_sample_static produce them -- are sorted and
+ * run-length encoded in HBM; words_out / counts_out receive the distinct words in
+ * ascending order and their counts, *nunique_out their number.  Tapes with more than
+ * 64 classical bits return QSB_ERR_UNSUPPORTED (use the per-shot words); more than
+ * max_unique distinct outcomes returns QSB_ERR_ARG with *nunique_out set.            */
+int32_t qsb_sample_counts(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
+                          int64_t shot_begin, int64_t shot_count, uint64_t* words_out, int64_t* counts_out,
+                          int64_t max_unique, int64_t* nunique_out);
+
 /* observe(): E[p] = sum_t coef[t] * <psi(params[p])| P_t |psi(params[p])>, the caller-
  * side composition of statevector + expval_pauli (suites.py:319-323).  term_out
  * (nullable) receives [npoints][nterms] single-term expectations.                    */

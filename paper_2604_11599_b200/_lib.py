@@ -104,6 +104,7 @@ _SIGS = {
                                   ctypes.POINTER(_I32)]),
     "qsb_statevector": (_I32, [_P, _P, _P]),
     "qsb_sample_static": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P]),
+    "qsb_sample_counts": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P, _P, _I64, ctypes.POINTER(_I64)]),
     "qsb_observe": (_I32, [_P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P, _P]),
     "qsb_debug_rng": (_I32, [_P, _U64, _I64, _I32, _P]),
     "qsb_plan_summary": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P]),

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -75,6 +76,7 @@ struct qsb_ctx_s {
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
   int64_t opt_dedup = 1, opt_reg_bits = 4;
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
+  DevBuf shotwords, histo;  // device-side shot histogram (qsb_sample_counts)
   qsb_stats last{};
   double run_flops = 0;  // floating-point work of the pass kernels in the current run
   bool run_physical = false;  // dedup ran: bytes / flops come from the device counters
@@ -922,9 +924,15 @@ int32_t qsb_tape_is_dynamic(qsb_tape tp, int32_t* out) {
   return QSB_OK;
 }
 
-int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
-                                int64_t shot_begin, int64_t shot_count, const double* predrawn,
-                                int32_t predrawn_stride, uint64_t* bits_out, int32_t* shot_status) {
+}  // extern "C"
+
+namespace {
+
+// Per-shot classical words of `shot_count` trajectories: into host memory (bits_out) or
+// left on the device (dev_out, [shot_count][nwords]) for the device-side histogram.
+int sample_traj_impl(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
+                     int64_t shot_count, const double* predrawn, int32_t predrawn_stride, uint64_t* bits_out,
+                     uint64_t* dev_out, int32_t* shot_status) {
   if (shot_count < 1) return fail(QSB_ERR_SIM, "shots must be >= 1");
   qsb_ctx ctx = tp->ctx;
   DeviceGuard g(ctx->device);
@@ -965,14 +973,15 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
     a.shot_begin = shot_begin;
     a.count = shot_count;
     a.predrawn = d_pre;
-    a.bits_out = ctx->bits.as<uint64_t>();
+    a.bits_out = dev_out ? dev_out : ctx->bits.as<uint64_t>();
     a.status_out = ctx->status.as<int32_t>();
     a.tie_count = ctx->counters.as<unsigned long long>();
     a.gate_count = ctx->counters.as<unsigned long long>() + 1;
     a.c64 = c64;
     QSB_CUDA(launch_resident(a, ctx->num_sms, ctx->stream));
-    QSB_CUDA(cudaMemcpyAsync(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost,
-                             ctx->stream));
+    if (!dev_out)
+      QSB_CUDA(cudaMemcpyAsync(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost,
+                               ctx->stream));
     QSB_CUDA(cudaMemcpyAsync(status.data(), ctx->status.p, sizeof(int32_t) * shot_count, cudaMemcpyDeviceToHost,
                              ctx->stream));
     float ms = timer.stop();
@@ -993,12 +1002,14 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
                   nullptr, 0, nullptr};
       rc = run_stream(ctx, r);
       if (rc) return rc;
-      QSB_CUDA(cudaMemcpyAsync(bits_out + off * t.nwords, ctx->bits.p, sizeof(uint64_t) * t.nwords * b,
-                               cudaMemcpyDeviceToHost, ctx->stream));
-      std::vector<TrajCtl> ctl((size_t)b);
-      QSB_CUDA(cudaMemcpyAsync(ctl.data(), ctx->ctl.p, sizeof(TrajCtl) * b, cudaMemcpyDeviceToHost, ctx->stream));
+      QSB_CUDA(cudaMemcpyAsync(dev_out ? dev_out + off * t.nwords : bits_out + off * t.nwords, ctx->bits.p,
+                               sizeof(uint64_t) * t.nwords * b,
+                               dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+      // only the 4-byte status field of each control block crosses PCIe (strided copy)
+      QSB_CUDA(cudaMemcpy2DAsync(status.data() + off, sizeof(int32_t),
+                                 ctx->ctl.as<char>() + offsetof(TrajCtl, status), sizeof(TrajCtl), sizeof(int32_t),
+                                 (size_t)b, cudaMemcpyDeviceToHost, ctx->stream));
       QSB_CUDA(cudaStreamSynchronize(ctx->stream));
-      for (int64_t i = 0; i < b; ++i) status[off + i] = ctl[i].status;
       pass_ms += pass_ms_sum(ctx, pd->plan.passes.size());
       pass_bytes += r.pass_bytes;
       passes += r.passes;
@@ -1020,6 +1031,17 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
   if (worst == QSB_ERR_PREDRAWN) return fail(worst, "pre-drawn uniform stream exhausted");
   if (worst != QSB_OK) return fail(worst, "trajectory failed");
   return QSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
+                                int64_t shot_begin, int64_t shot_count, const double* predrawn,
+                                int32_t predrawn_stride, uint64_t* bits_out, int32_t* shot_status) {
+  return sample_traj_impl(tp, precision, params, seed, shot_begin, shot_count, predrawn, predrawn_stride, bits_out,
+                          nullptr, shot_status);
 }
 
 int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params, uint64_t* rng_state, uint64_t seed,
@@ -1194,8 +1216,12 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
   return QSB_OK;
 }
 
-int32_t qsb_sample_static(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
-                          int64_t shot_count, uint64_t* bits_out) {
+}  // extern "C"
+
+namespace {
+
+int sample_static_impl(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
+                       int64_t shot_count, uint64_t* bits_out, uint64_t* dev_out) {
   if (shot_count < 1) return fail(QSB_ERR_SIM, "shots must be >= 1");
   const TapeInfo& t = tp->info;
   if (t.needs_trajectories) return fail(QSB_ERR_ARG, "tape needs trajectories");
@@ -1232,11 +1258,62 @@ int32_t qsb_sample_static(qsb_tape tp, int32_t precision, const double* params, 
   }
   launch_cumsum_seq(st->c64, st->amps.p, t.n, ctx->misc.as<double>(), ctx->stream);
   launch_static_search(ctx->misc.as<double>(), t.n, seed, shot_begin, shot_count, d_mq, d_mb, (int)mq.size(), t.nwords,
-                       d_bits, ctx->stream);
-  e = cudaMemcpyAsync(bits_out, d_bits, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost, ctx->stream);
+                       dev_out ? dev_out : d_bits, ctx->stream);
+  e = cudaSuccess;
+  if (!dev_out)
+    e = cudaMemcpyAsync(bits_out, d_bits, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   qsb_state_destroy(st);
   if (e != cudaSuccess) return fail(QSB_ERR_CUDA, cudaGetErrorString(e));
+  return check_sticky();
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t qsb_sample_static(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
+                          int64_t shot_count, uint64_t* bits_out) {
+  return sample_static_impl(tp, precision, params, seed, shot_begin, shot_count, bits_out, nullptr);
+}
+
+int32_t qsb_sample_counts(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
+                          int64_t shot_count, uint64_t* words_out, int64_t* counts_out, int64_t max_unique,
+                          int64_t* nunique_out) {
+  if (shot_count < 1) return fail(QSB_ERR_SIM, "shots must be >= 1");
+  const TapeInfo& t = tp->info;
+  if (t.nwords != 1) return fail(QSB_ERR_UNSUPPORTED, "device histogram needs <= 64 classical bits");
+  if (shot_count > INT32_MAX) return fail(QSB_ERR_ARG, "device histogram: at most 2^31-1 shots per call");
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  const size_t n = (size_t)shot_count;
+  const size_t scratch = hist_scratch_bytes(n);
+  QSB_CUDA(ctx->shotwords.ensure(sizeof(uint64_t) * n));
+  QSB_CUDA(ctx->histo.ensure(sizeof(uint64_t) * n + sizeof(int32_t) * n + sizeof(uint64_t) * n + 64 + scratch));
+  uint64_t* d_words = ctx->shotwords.as<uint64_t>();
+  int rc = t.needs_trajectories
+               ? sample_traj_impl(tp, precision, params, seed, shot_begin, shot_count, nullptr, 0, nullptr, d_words,
+                                  nullptr)
+               : sample_static_impl(tp, precision, params, seed, shot_begin, shot_count, nullptr, d_words);
+  if (rc) return rc;
+  char* hb = ctx->histo.as<char>();
+  uint64_t* d_uniq = reinterpret_cast<uint64_t*>(hb);
+  int32_t* d_counts = reinterpret_cast<int32_t*>(d_uniq + n);
+  uint64_t* d_sorted = reinterpret_cast<uint64_t*>(d_counts + n + (n & 1));
+  int32_t* d_nruns = reinterpret_cast<int32_t*>(d_sorted + n);
+  void* d_scratch = reinterpret_cast<char*>(d_nruns) + 64;
+  QSB_CUDA(launch_histogram(d_words, d_sorted, n, std::max(1, t.nbits), d_uniq, d_counts, d_nruns, d_scratch, scratch,
+                            ctx->stream));
+  int32_t nr = 0;
+  QSB_CUDA(cudaMemcpyAsync(&nr, d_nruns, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *nunique_out = nr;
+  if (nr > max_unique) return fail(QSB_ERR_ARG, "more distinct outcomes than max_unique (see nunique_out)");
+  std::vector<int32_t> c32((size_t)nr);
+  QSB_CUDA(cudaMemcpyAsync(words_out, d_uniq, sizeof(uint64_t) * nr, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaMemcpyAsync(c32.data(), d_counts, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int32_t i = 0; i < nr; ++i) counts_out[i] = c32[i];
   return check_sticky();
 }
 

@@ -50,6 +50,12 @@ void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const
 void launch_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
                                const ExpvalTerm* terms_by_out, double* out, cudaStream_t s);
 
+// device-side shot histogram (qsb_hist.cu): sort the per-shot words on their low
+// `nbits` bits and run-length encode -> ascending distinct words + counts
+size_t hist_scratch_bytes(size_t n);
+cudaError_t launch_histogram(const uint64_t* words, uint64_t* sorted, size_t n, int nbits, uint64_t* uniq,
+                             int32_t* counts, int32_t* nruns, void* scratch, size_t scratch_bytes, cudaStream_t s);
+
 // static sampling
 void launch_cumsum_seq(int c64, const void* amps, int n, double* cdf, cudaStream_t s);
 void launch_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,

@@ -37,6 +37,11 @@ def _gpu_counts(bound, shots, seed, shot_begin, precision, device):
 
     if shots <= 0:
         return Counter()
+    tape = sim.compile_tape(bound.kernel, device)
+    if tape.nwords == 1:  # histogram built on the device; only distinct outcomes come back
+        uniq, counts = sim.sample_counts(bound, shots, seed, shot_begin=shot_begin, precision=precision, device=device)
+        keys = tape.keys(uniq) if tape.nbits else [""] * len(uniq)
+        return Counter({k: int(c) for k, c in zip(keys, counts)})
     words, tape = sim.sample_words(bound, shots, seed, shot_begin=shot_begin, precision=precision, device=device)
     return Counter(sim.histogram_from_words(tape, words, shots).counts)
 

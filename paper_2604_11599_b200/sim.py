@@ -704,8 +704,37 @@ def sample(bound, shots: int, seed: int, workers: int = 1, *, precision=None, de
     batch layout cannot change the result)."""
     if shots < 1:
         raise SimError("shots must be >= 1")
+    tape = compile_tape(bound.kernel, device)
+    if tape.nwords == 1:
+        uniq, counts = sample_counts(bound, shots, seed, precision=precision, device=device)
+        keys = tape.keys(uniq) if tape.nbits else [""] * len(uniq)
+        return ShotHistogram({k: int(c) for k, c in zip(keys, counts)}, int(shots))
     words, tape = sample_words(bound, shots, seed, precision=precision, device=device)
     return histogram_from_words(tape, words, shots)
+
+
+def sample_counts(bound, shots: int, seed: int, *, shot_begin: int = 0, precision=None,
+                  device=None) -> tuple[np.ndarray, np.ndarray]:
+    """Distinct per-shot words (ascending) and their counts, histogrammed on the
+    device (qsb_sample_counts): only the distinct outcomes leave the GPU."""
+    if shots < 1:
+        raise SimError("shots must be >= 1")
+    tape = compile_tape(bound.kernel, device)
+    ctx = tape.ctx
+    params = tape.params(bound.values)
+    cap = min(int(shots), 1 << min(tape.nbits, 40))
+    while True:
+        uniq = np.zeros((cap, 1), dtype=np.uint64)
+        counts = np.zeros(cap, dtype=np.int64)
+        nu = ctypes.c_int64()
+        rc = ctx.lib.qsb_sample_counts(tape.handle, _prec(precision), _lib.ptr(params), int(seed) & _M64,
+                                       int(shot_begin), int(shots), _lib.ptr(uniq), _lib.ptr(counts), cap,
+                                       ctypes.byref(nu))
+        if rc == _lib.ERR_ARG and nu.value > cap:  # pragma: no cover - cap >= shots >= distinct outcomes
+            cap = nu.value
+            continue
+        _lib.check(rc)
+        return uniq[:nu.value], counts[:nu.value]
 
 
 def statevector(bound, *, precision=None, device=None) -> StateVector:

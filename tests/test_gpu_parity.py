@@ -358,3 +358,27 @@ def test_qft_matches_dft():
             want = np.exp(2j * math.pi * j / (1 << n)) / math.sqrt(1 << n)
             fid = abs(np.vdot(st.amps, want)) ** 2
             assert fid > 1 - 1e-10
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_device_histogram_matches_per_shot_words(golden, prec):
+    """qsb_sample_counts (sort + run-length encode in HBM) == the histogram of the
+    per-shot words, for the trajectory path, the static path and a bitless kernel."""
+    _, kd = workloads.dyn_circuit(n=14, layers=10, every=5, nmeas=3, seed=41)
+    cases = [ir.bind(kd, [])]
+    cases += [ir.bind(ir.kernel_from_json(c["kernel"]), []) for c in golden("static_sampling.json")]
+    cases.append(ir.bind(ir.Kernel(2, [("q", 2)], [], [], [ir.Gate("h", (), (0,), ())]), []))
+    for b in cases:
+        words, tape = sim.sample_words(b, 700, 99, shot_begin=5, precision=prec)
+        uniq, counts = sim.sample_counts(b, 700, 99, shot_begin=5, precision=prec)
+        w, c = np.unique(words[:, 0], return_counts=True)
+        np.testing.assert_array_equal(uniq[:, 0], w)
+        np.testing.assert_array_equal(counts, c)
+        assert counts.sum() == 700
+        w0, _ = sim.sample_words(b, 700, 99, precision=prec)
+        assert sim.sample(b, 700, 99, precision=prec).counts == sim.histogram_from_words(tape, w0, 700).counts
+    # sample() goes through the device histogram and still matches the reference goldens
+    for name, case in golden("ff_suite.json").items():
+        b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
+        if prec == "c128":
+            assert sim.sample(b, 1024, 1234).counts == case["hist_1024_seed1234"], name
