@@ -120,14 +120,24 @@ int tile_qubits(qsb_ctx ctx, int c64) {
 }
 int low_qubits(int c64) { return c64 ? 5 : 4; }  // 256-byte contiguous runs
 
+// Blocking copy ordered on the context's stream.  ctx->stream is non-blocking, so a plain
+// cudaMemcpy (legacy stream) neither waits for work queued on it nor -- for pageable
+// host-to-device copies -- guarantees the bytes have landed when it returns; a kernel
+// launched next on ctx->stream could read the destination early.
+cudaError_t copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
 int upload_tape_device(qsb_tape tp) {
   TapeInfo& t = tp->info;
   QSB_CUDA(tp->d_dev.ensure(std::max<size_t>(1, t.dev.size()) * sizeof(DevOp)));
   if (!t.dev.empty())
-    QSB_CUDA(cudaMemcpy(tp->d_dev.p, t.dev.data(), t.dev.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(tp->d_dev.p, t.dev.data(), t.dev.size() * sizeof(DevOp), cudaMemcpyHostToDevice, tp->ctx->stream));
   QSB_CUDA(tp->d_matsrc.ensure(std::max<size_t>(1, t.mats.size()) * sizeof(MatSrc)));
   if (!t.mats.empty())
-    QSB_CUDA(cudaMemcpy(tp->d_matsrc.p, t.mats.data(), t.mats.size() * sizeof(MatSrc), cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(tp->d_matsrc.p, t.mats.data(), t.mats.size() * sizeof(MatSrc), cudaMemcpyHostToDevice, tp->ctx->stream));
   QSB_CUDA(tp->d_mats.ensure(std::max<size_t>(1, t.mats.size()) * 8 * sizeof(double)));
   if (!t.mats.empty() && !t.has_param_angles) {
     launch_mats_prep(tp->d_matsrc.as<MatSrc>(), (int)t.mats.size(), nullptr, 0, 1, tp->d_mats.as<double>(),
@@ -155,20 +165,20 @@ int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
   StreamPlan& P = pd->plan;
   QSB_CUDA(pd->gates.ensure(std::max<size_t>(1, P.gates.size()) * sizeof(PassGate)));
   if (!P.gates.empty())
-    QSB_CUDA(cudaMemcpy(pd->gates.p, P.gates.data(), P.gates.size() * sizeof(PassGate), cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(pd->gates.p, P.gates.data(), P.gates.size() * sizeof(PassGate), cudaMemcpyHostToDevice, tp->ctx->stream));
   QSB_CUDA(pd->rops.ensure(std::max<size_t>(1, P.region_ops.size()) * sizeof(DevOp)));
   if (!P.region_ops.empty())
-    QSB_CUDA(cudaMemcpy(pd->rops.p, P.region_ops.data(), P.region_ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(pd->rops.p, P.region_ops.data(), P.region_ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice, tp->ctx->stream));
   QSB_CUDA(pd->guard_gates.ensure(std::max<size_t>(1, P.guard_gates.size()) * sizeof(int32_t)));
-  QSB_CUDA(cudaMemcpy(pd->guard_gates.p, P.guard_gates.data(), P.guard_gates.size() * sizeof(int32_t),
-                      cudaMemcpyHostToDevice));
+  QSB_CUDA(copy_sync(pd->guard_gates.p, P.guard_gates.data(), P.guard_gates.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice, tp->ctx->stream));
   QSB_CUDA(pd->phases.ensure(std::max<size_t>(1, P.phases.size()) * sizeof(PhaseDesc)));
   if (!P.phases.empty())
-    QSB_CUDA(cudaMemcpy(pd->phases.p, P.phases.data(), P.phases.size() * sizeof(PhaseDesc), cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(pd->phases.p, P.phases.data(), P.phases.size() * sizeof(PhaseDesc), cudaMemcpyHostToDevice, tp->ctx->stream));
   QSB_CUDA(pd->phase_gates.ensure(std::max<size_t>(1, P.phase_gates.size()) * sizeof(PhaseGate)));
   if (!P.phase_gates.empty())
-    QSB_CUDA(cudaMemcpy(pd->phase_gates.p, P.phase_gates.data(), P.phase_gates.size() * sizeof(PhaseGate),
-                        cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(pd->phase_gates.p, P.phase_gates.data(), P.phase_gates.size() * sizeof(PhaseGate),
+                        cudaMemcpyHostToDevice, tp->ctx->stream));
   pd->pflops.assign(P.passes.size(), 0.0);
   for (size_t i = 0; i < P.passes.size(); ++i)
     if (P.passes[i].phase_count) pd->pflops[i] = pass_flops(tp->info, P, (int)i);
@@ -403,7 +413,7 @@ int64_t pick_batch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, int c64,
 int finish_stats(qsb_ctx ctx, float total_ms, double pass_ms, double pass_bytes, int64_t passes, int64_t decides,
                  int64_t launches, int engine, int k) {
   unsigned long long cnt[4] = {0, 0, 0, 0};
-  QSB_CUDA(cudaMemcpy(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+  QSB_CUDA(copy_sync(cnt, ctx->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->stream));
   if (ctx->run_physical) {  // history dedup: what the kernels actually moved / computed
     double phys[2];
     std::memcpy(phys, &cnt[2], sizeof(phys));
@@ -1139,22 +1149,22 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
     rc = check_sticky();
     if (rc) return rc;
     status = c.status;
-    QSB_CUDA(cudaMemcpy(d_rng, c.rng, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice));
-    QSB_CUDA(cudaMemcpy(d_draws, &c.draws, sizeof(int32_t), cudaMemcpyHostToDevice));
+    QSB_CUDA(copy_sync(d_rng, c.rng, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    QSB_CUDA(copy_sync(d_draws, &c.draws, sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
     finish_stats(ctx, ms, pass_ms_sum(ctx, pd->plan.passes.size()), r.pass_bytes, r.passes, r.decides, r.launches + 1,
                  1, pd->plan.k);
     note_jit(ctx, pd);
   }
-  QSB_CUDA(cudaMemcpy(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords, cudaMemcpyDeviceToHost));
+  QSB_CUDA(copy_sync(bits_out, ctx->bits.p, sizeof(uint64_t) * t.nwords, cudaMemcpyDeviceToHost, ctx->stream));
   int32_t nt2[2] = {0, 0};
-  QSB_CUDA(cudaMemcpy(nt2, d_ntrace, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  QSB_CUDA(copy_sync(nt2, d_ntrace, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
   int32_t nt = nt2[0];
   if (ntrace) *ntrace = nt;
   if (ndraws) *ndraws = nt2[1];
-  if (rng_state) QSB_CUDA(cudaMemcpy(rng_state, d_rng, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (rng_state) QSB_CUDA(copy_sync(rng_state, d_rng, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
   if (trace_out && nt > 0)
-    QSB_CUDA(cudaMemcpy(trace_out, d_trace, sizeof(int64_t) * std::min(nt, max_trace) * (2 + t.nwords),
-                        cudaMemcpyDeviceToHost));
+    QSB_CUDA(copy_sync(trace_out, d_trace, sizeof(int64_t) * std::min(nt, max_trace) * (2 + t.nwords),
+                        cudaMemcpyDeviceToHost, ctx->stream));
   if (status == QSB_ERR_DEGENERATE) return fail(status, "selected measurement branch has probability < 1e-15");
   if (status == QSB_ERR_PREDRAWN) return fail(status, "pre-drawn uniform stream exhausted");
   if (status != QSB_OK) return fail(status, "trajectory failed");
