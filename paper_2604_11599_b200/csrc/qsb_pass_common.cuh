@@ -86,14 +86,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-__device__ __forceinline__ void prefetch_l2(const void* gmem, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gmem), "r"(bytes));
-}
-
 // Buffering mode: complex64 tiles (32 KiB) double-buffer in shared memory (two CTAs per
 // SM still fit); complex128 tiles (64 KiB) keep one buffer so that two CTAs share an SM,
-// and the next item is bulk-prefetched into L2 (TMA prefetch) while the current one
-// computes, so its gather hits L2.
+// and the next item is prefetched into L2 (one prefetch.global.L2 per 128-byte line,
+// issued per thread: the bulk TMA prefetch takes a warp-uniform address and compiled
+// to a 32-iteration loop per warp) while the current one computes, so its gather hits L2.
 __host__ __device__ inline int pass_buffers(int c64) { return c64 ? 2 : 1; }
 
 // dynamic shared memory of a register-blocked pass
@@ -102,7 +99,11 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
   const size_t amp = c64 ? 8 : 16;
   const size_t sgate = c64 ? 64 : 96;
   return pass_buffers(c64) * (amp << pd.k) + sgate * pd.pgate_count + (sizeof(uint64_t) << (pd.k - pd.lowq)) +
-         (sizeof(uint32_t) << (pd.k - sb)) + sizeof(double) * (1u << (pd.k - rb));
+         (sizeof(uint32_t) << (pd.k - sb)) + sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb);
+}
+
+__device__ __forceinline__ void prefetch_line_l2(const void* gmem) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gmem));
 }
 
 template <typename R, int RB, typename PhaseRunner>
@@ -117,6 +118,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   uint64_t* hi_off = reinterpret_cast<uint64_t*>(sg + pd.pgate_count);
   uint32_t* swz = reinterpret_cast<uint32_t*>(hi_off + (TL >> pd.lowq));
   double* red = reinterpret_cast<double*>(swz + (TL >> SB));
+  uint32_t* ujt = reinterpret_cast<uint32_t*>(red + T);  // [2^RB] swizzled slot of j*T
   const uint64_t lowm = (1ull << pd.lowq) - 1;
   const uint64_t shi = pd.smask & ~lowm;
   for (int h = tid; h < (TL >> pd.lowq); h += T) hi_off[h] = pdep64((uint64_t)h, shi);
@@ -128,16 +130,37 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     swz[h] = s;
   }
   __syncthreads();
+  // Tile element l = tid + j*T (j < 2^RB; tid and j*T occupy disjoint bits, and
+  // T is a multiple of 2^lowq and of 2^SB).  pdep and the swizzle are both linear
+  // over disjoint bit fields, so
+  //   physical offset  = base_phys | Pt | hi_off[j * (T >> lowq)]
+  //   swizzled slot    = St ^ ujt[j]            (St = tid ^ swz[tid >> SB])
+  // and with the Pauli-X frame flip fl of an item the slot of l ^ fl is
+  //   (Ft ^ G) ^ ujt[j], Ft = swizzled slot of tid ^ (fl & (T-1)), G = that of fl & ~(T-1).
+  // The loops below therefore cost a few integer ops per amplitude.
+  if (tid < (1 << RB)) ujt[tid] = swz_slot<SB>(swz, (uint32_t)(tid * T));
+  const uint64_t Pt = ((uint64_t)tid & lowm) | hi_off[tid >> pd.lowq];
+  const uint32_t St = swz_slot<SB>(swz, (uint32_t)tid);
+  const int hstep = T >> pd.lowq;
+  __syncthreads();
   const int ntl = a.n - k;
   const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << ntl;
   const uint64_t qmask = (a.n >= 64) ? ~0ull : ((1ull << a.n) - 1);
 
+  // swizzled-slot base of this thread for an item with frame flip fl
+  auto flip_base = [&](uint32_t fl) -> uint32_t {
+    return swz_slot<SB>(swz, (uint32_t)tid ^ (fl & (uint32_t)(T - 1))) ^ swz_slot<SB>(swz, fl & ~(uint32_t)(T - 1));
+  };
+
   auto prefetch = [&](const PassItem& it, A* dst) {
     if (!it.alive) return;
     const A* st = reinterpret_cast<const A*>(a.state) + (it.slot << a.n);
-    for (int l = tid; l < TL; l += T) {
-      A* d = dst + swz_slot<SB>(swz, (uint32_t)l ^ it.fl);
-      const uint64_t p = it.base_phys | ((uint64_t)l & lowm) | hi_off[l >> pd.lowq];
+    const uint64_t pb = it.base_phys | Pt;
+    const uint32_t fb = flip_base(it.fl);
+#pragma unroll 4
+    for (int j = 0; j < (1 << RB); ++j) {
+      A* d = dst + (fb ^ ujt[j]);
+      const uint64_t p = pb | hi_off[j * hstep];
       if (pd.init_zero) {
         *d = mk<R>(p == 0 ? (R)1 : (R)0, (R)0);
       } else if (sizeof(A) == 16) {
@@ -148,11 +171,14 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     }
   };
 
-  auto prefetch_next_l2 = [&](const PassItem& it) {  // one 2^lowq-amplitude run per thread
+  auto prefetch_next_l2 = [&](const PassItem& it) {  // the 128-byte lines of one 2^lowq run per thread
     if (!it.alive || pd.init_zero) return;
-    const A* st = reinterpret_cast<const A*>(a.state) + (it.slot << a.n);
-    for (int h = tid; h < (TL >> pd.lowq); h += T)
-      prefetch_l2(st + (it.base_phys | hi_off[h]), (unsigned)(sizeof(A) << pd.lowq));
+    const char* st = reinterpret_cast<const char*>(reinterpret_cast<const A*>(a.state) + (it.slot << a.n));
+    const unsigned run = (unsigned)(sizeof(A) << pd.lowq);
+    for (int h = tid; h < (TL >> pd.lowq); h += T) {
+      const char* r0 = st + sizeof(A) * (it.base_phys | hi_off[h]);
+      for (unsigned o = 0; o < run; o += 128) prefetch_line_l2(r0 + o);
+    }
   };
 
   int64_t w = blockIdx.x;
@@ -184,9 +210,11 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     if (it.alive) {
       if (it.pending) {  // collapse of the previous decide: projection + complex scale
         const R sre = (R)it.sre, sim = (R)it.sim;
-        for (int l = tid; l < TL; l += T) {
-          const uint64_t p = it.base_phys | ((uint64_t)l & lowm) | hi_off[l >> pd.lowq];
-          A* d = tile + swz_slot<SB>(swz, (uint32_t)l ^ it.fl);
+        const uint64_t pb = it.base_phys | Pt;
+        const uint32_t fb = flip_base(it.fl);
+        for (int j = 0; j < (1 << RB); ++j) {
+          const uint64_t p = pb | hi_off[j * hstep];
+          A* d = tile + (fb ^ ujt[j]);
           A v = *d;
           if ((p & it.Kp) != it.Vp) v = mk<R>(0, 0);
           else v = mk<R>(fma(sre, v.x, -sim * v.y), fma(sre, v.y, sim * v.x));
@@ -281,10 +309,9 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
         }
       }
       A* st = reinterpret_cast<A*>(a.state) + (it.slot << a.n);
-      for (int l = tid; l < TL; l += T) {
-        uint64_t p = it.base_phys | ((uint64_t)l & lowm) | hi_off[l >> pd.lowq];
-        st[p] = tile[swz_slot<SB>(swz, (uint32_t)l)];
-      }
+      const uint64_t pb = it.base_phys | Pt;
+#pragma unroll 4
+      for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = tile[St ^ ujt[j]];
     }
     __syncthreads();
     if (NB == 2) b ^= 1;
