@@ -259,7 +259,13 @@ struct Planner {
         uint32_t need = 0;
         if (g.gclass == GC_DENSE || g.gclass == GC_XPERM || g.gclass == GC_ANTI) need = 1u << g.lt;
         need &= ~R;
-        if (popc(R | need) <= rb) {
+        // tile controls of a register-target gate: in the registers the controlled pairs
+        // are chosen at compile time; on a thread position every pair costs selects
+        const uint32_t want = need ? (need | (g.lcm & ~R)) : 0;
+        if (want && popc(R | want) <= rb) {
+          R |= want;
+          take.push_back(gi);
+        } else if (popc(R | need) <= rb) {
           R |= need;
           take.push_back(gi);
         } else {
