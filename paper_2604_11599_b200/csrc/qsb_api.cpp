@@ -760,6 +760,8 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   for (int t : diag) groups[0].terms.push_back(t);
   std::vector<ExpvalTerm> dev_terms, by_out(nterm);
   std::vector<ExpvalGroup> dev_groups;
+  std::vector<EvMap> dev_maps;
+  const int sb = c64 ? 4 : 3;
   for (Grp& g : groups) {
     for (int q = 0; q < n && __builtin_popcountll(g.S) < k; ++q) g.S |= 1ull << q;
     ExpvalGroup eg{};
@@ -775,7 +777,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
         if (m & (s & (~s + 1))) out |= 1u << j;
       return out;
     };
-    for (int t : g.terms) {
+    auto make_term = [&](int t) {
       ExpvalTerm e{};
       e.xl = compress(xm[t]);
       e.zl = compress(zm[t] & g.S);
@@ -783,26 +785,102 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
       e.zg = zm[t] & ~g.S;
       e.ny = ny[t];
       e.out = t;
-      dev_terms.push_back(e);
-      by_out[t] = e;
+      return e;
+    };
+    if (k == 12) {
+      // register mappings: first-fit of each term's X support (tile positions) into
+      // sets of <= 4 positions; per mapping, the 16 registers span those positions
+      struct Map { uint32_t U; std::vector<int> terms; };
+      std::vector<Map> maps;
+      std::vector<int> wide;  // > 4 X letters in the tile: pair-loop kernel
+      for (int t : g.terms) {
+        const uint32_t xl = compress(xm[t]);
+        if (__builtin_popcount(xl) > 4) {
+          wide.push_back(t);
+          continue;
+        }
+        bool placed = false;
+        for (Map& m : maps)
+          if (__builtin_popcount(m.U | xl) <= 4) {
+            m.U |= xl;
+            m.terms.push_back(t);
+            placed = true;
+            break;
+          }
+        if (!placed) maps.push_back({xl, {t}});
+      }
+      eg.map_begin = (int)dev_maps.size();
+      eg.nmap = (int)maps.size();
+      for (Map& m : maps) {
+        int rpos[4], nr = 0;
+        for (int p = 0; p < k && nr < 4; ++p)
+          if (m.U >> p & 1) rpos[nr++] = p;
+        for (int p = 0; p < k && nr < 4; ++p)
+          if (!(m.U >> p & 1)) rpos[nr++] = p;
+        EvMap em{};
+        tile_mapping(rpos, 4, k, sb, em.tpos, em.soff);
+        em.term_begin = (int)dev_terms.size();
+        em.nterm = (int)m.terms.size();
+        for (int t : m.terms) {
+          ExpvalTerm e = make_term(t);
+          for (int b = 0; b < 4; ++b)
+            if (e.xl >> rpos[b] & 1) e.xr |= 1u << b;
+          for (int j = 0; j < 16; ++j) {
+            uint32_t pos = 0;
+            for (int b = 0; b < 4; ++b)
+              if (j >> b & 1) pos |= 1u << rpos[b];
+            if (__builtin_popcount(pos & e.zl) & 1) e.zsig |= 1u << j;
+          }
+          dev_terms.push_back(e);
+          by_out[t] = e;
+        }
+        dev_maps.push_back(em);
+      }
+      eg.nterm = (int)dev_terms.size() - eg.term_begin;
+      if (!wide.empty()) {
+        if (eg.nterm) dev_groups.push_back(eg);
+        eg = ExpvalGroup{};
+        eg.smask = g.S;
+        eg.k = k;
+        eg.lowq = lowq;
+        eg.term_begin = (int)dev_terms.size();
+        eg.nterm = (int)wide.size();
+        for (int t : wide) {
+          ExpvalTerm e = make_term(t);
+          dev_terms.push_back(e);
+          by_out[t] = e;
+        }
+      }
+    } else {
+      for (int t : g.terms) {
+        ExpvalTerm e = make_term(t);
+        dev_terms.push_back(e);
+        by_out[t] = e;
+      }
     }
     dev_groups.push_back(eg);
   }
   const int ntl = n - k;
   const size_t pbytes = sizeof(double) * (size_t)slots * nterm * ((size_t)1 << ntl);
   QSB_CUDA(ctx->misc.ensure(pbytes + 64));
-  QSB_CUDA(ctx->misc2.ensure(sizeof(ExpvalTerm) * 2 * (nterm + 1) + sizeof(double) * nterm * slots + 64));
+  QSB_CUDA(ctx->misc2.ensure(sizeof(ExpvalTerm) * 2 * (nterm + 1) + sizeof(double) * nterm * slots +
+                              sizeof(EvMap) * (dev_maps.size() + 1) + 64));
   char* base = ctx->misc2.as<char>();
   ExpvalTerm* d_terms = reinterpret_cast<ExpvalTerm*>(base);
   ExpvalTerm* d_byout = d_terms + (nterm + 1);
   double* d_out = reinterpret_cast<double*>(d_byout + (nterm + 1));
+  EvMap* d_maps = reinterpret_cast<EvMap*>(d_out + nterm * slots);
+  if (!dev_maps.empty())
+    QSB_CUDA(cudaMemcpyAsync(d_maps, dev_maps.data(), sizeof(EvMap) * dev_maps.size(), cudaMemcpyHostToDevice,
+                             ctx->stream));
   if (nterm) {
     QSB_CUDA(cudaMemcpyAsync(d_terms, dev_terms.data(), sizeof(ExpvalTerm) * nterm, cudaMemcpyHostToDevice,
                              ctx->stream));
     QSB_CUDA(cudaMemcpyAsync(d_byout, by_out.data(), sizeof(ExpvalTerm) * nterm, cudaMemcpyHostToDevice, ctx->stream));
   }
   for (const ExpvalGroup& g : dev_groups)
-    if (g.nterm) launch_expval_tile(c64, amps, n, slots, g, d_terms, ctx->misc.as<double>(), nterm, ctx->stream);
+    if (g.nterm)
+      launch_expval_tile(c64, amps, n, slots, g, d_terms, d_maps, ctx->misc.as<double>(), nterm, ctx->stream);
   QSB_CUDA(cudaGetLastError());
   launch_expval_tile_finish(ctx->misc.as<double>(), slots, nterm, ntl, d_byout, d_out, ctx->stream);
   QSB_CUDA(cudaMemcpyAsync(out_host, d_out, sizeof(double) * nterm * slots, cudaMemcpyDeviceToHost, ctx->stream));

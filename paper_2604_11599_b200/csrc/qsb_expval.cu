@@ -5,20 +5,35 @@
 // The terms are grouped on the host so that each group's X supports fit in one tile
 // qubit set S (k qubits, always containing the low qubits for 32-byte runs); one launch
 // per group reads every tile of every state exactly once and evaluates all of the
-// group's terms from shared memory: pairs (l, l ^ x_local) stay inside the tile, Z/Y
-// signs of the out-of-tile qubits are one per-tile sign.  Diagonal (Z-only) terms ride
-// along with the first group.  The per-grid reduction is fixed-order (warp shfl_down,
-// warp partials summed in order, tiles summed in order) -- deterministic.
+// group's terms on chip: pairs (l, l ^ x_local) stay inside the tile, Z/Y signs of the
+// out-of-tile qubits are one per-tile sign.  Diagonal (Z-only) terms ride along with
+// the first group.
+//
+// Full 12-qubit tiles use the register-mapped kernel: the group's terms are split into
+// mappings whose X supports together fit in 4 tile positions; per mapping every thread
+// loads the 16 amplitudes that differ only in those positions from the (swizzled,
+// conflict-free) shared tile into registers, and every term of the mapping is then a
+// compile-time pair pattern over those registers (its X letters in register space,
+// its register Z signs a 16-bit mask) -- a few FP64 ops per pair, no shared-memory
+// traffic or index arithmetic per pair.  Smaller tiles (n < 12) use the pair loop.
+//
+// The reduction is fixed-order (warp shfl_down, warp partials summed in order, tiles
+// summed in order) -- deterministic, no atomics.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "qsb_device.cuh"
 #include "qsb_launch.h"
+#include "qsb_pass_common.cuh"
 
 namespace qsb {
 
 namespace {
 
 constexpr int kET = 256;
+
+// ---- pair-loop kernel (any tile size) -------------------------------------------
 
 template <typename R>
 __global__ void __launch_bounds__(kET) k_expval_tile(const typename Amp<R>::T* __restrict__ states, int n,
@@ -41,7 +56,6 @@ __global__ void __launch_bounds__(kET) k_expval_tile(const typename Amp<R>::T* _
   __syncthreads();
   for (int l = tid; l < TL; l += kET) tile[l] = st[base | ((uint64_t)l & lowm) | hi_off[l >> g.lowq]];
   __syncthreads();
-  const int ntiles_log2 = n - k;
   for (int t = 0; t < g.nterm; ++t) {
     const ExpvalTerm tm = terms[g.term_begin + t];
     double acc = 0.0;
@@ -69,18 +83,163 @@ __global__ void __launch_bounds__(kET) k_expval_tile(const typename Amp<R>::T* _
     double s = 0.0;
     for (int w = 0; w < kET / 32; ++w) s += wsum[t * (kET / 32) + w];
     if (__popcll(base & tm.zg) & 1) s = -s;
-    partial[((int64_t)slot * nterm_total + tm.out) * ((int64_t)1 << ntiles_log2) + blockIdx.x] = s;
+    partial[((int64_t)slot * gridDim.x + blockIdx.x) * nterm_total + tm.out] = s;
   }
 }
 
+// ---- register-mapped kernel (k = 12: 256 threads x 16 registers) -----------------
+
+// (-1)^(bit j of zsig) * x as one integer op on the sign bit
+__device__ __forceinline__ double flip_sign(double x, uint32_t zsig, int j) {
+  const int hi = __double2hiint(x) ^ (int)((zsig << (31 - j)) & 0x80000000u);
+  return __hiloint2double(hi, __double2loint(x));
+}
+
+// sum over the 8 register pairs (j, j ^ XR), j without XR's top bit, of the signed
+// Re / Im part of conj(v_j) v_{j ^ XR}; zsig bit j = Z sign of register j
+template <typename R, int XR>
+__device__ __forceinline__ double ev_pairs(const typename Amp<R>::T* v, uint32_t zsig, bool im) {
+  constexpr int TOP = 1 << (31 - __builtin_clz(XR));
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j & TOP) continue;
+    const double ur = v[j].x, ui = v[j].y, vr = v[j ^ XR].x, vi = v[j ^ XR].y;
+    const double val = im ? fma(ur, vi, -ui * vr) : fma(ur, vr, ui * vi);
+    acc += flip_sign(val, zsig, j);
+  }
+  return acc;
+}
+
+// empty asm with the amplitudes as in/out operands: the products of a term are not
+// loop-invariant for the compiler, so it cannot hoist all 15 pair patterns' products
+// out of the term loop (which spilled ~1.7 KB per thread)
+__device__ __forceinline__ void opaque(double2& a) { asm volatile("" : "+d"(a.x), "+d"(a.y)); }
+__device__ __forceinline__ void opaque(float2& a) { asm volatile("" : "+f"(a.x), "+f"(a.y)); }
+
+template <typename R>
+__device__ __forceinline__ double ev_term(const typename Amp<R>::T* v, uint32_t xr, uint32_t zsig, bool im) {
+  switch (xr) {
+    case 0: {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc += flip_sign(norm2<R>(v[j]), zsig, j);
+      return acc;
+    }
+#define QSB_EV_CASE(X) \
+  case X: return ev_pairs<R, X>(v, zsig, im);
+    QSB_EV_CASE(1) QSB_EV_CASE(2) QSB_EV_CASE(3) QSB_EV_CASE(4) QSB_EV_CASE(5) QSB_EV_CASE(6) QSB_EV_CASE(7)
+    QSB_EV_CASE(8) QSB_EV_CASE(9) QSB_EV_CASE(10) QSB_EV_CASE(11) QSB_EV_CASE(12) QSB_EV_CASE(13) QSB_EV_CASE(14)
+    QSB_EV_CASE(15)
+#undef QSB_EV_CASE
+    default: return 0.0;
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kET, 2) k_expval_reg(const typename Amp<R>::T* __restrict__ states, int n,
+                                                      int64_t slots, ExpvalGroup g,
+                                                      const ExpvalTerm* __restrict__ terms,
+                                                      const EvMap* __restrict__ maps, double* __restrict__ partial,
+                                                      int nterm_total) {
+  // persistent: the per-CTA tables are built once, then the CTA walks (slot, tile)
+  // items with a grid stride, prefetching the next item's runs into L2 while the
+  // current one is evaluated
+  using A = typename Amp<R>::T;
+  constexpr int SB = sizeof(R) == 8 ? 3 : 4;
+  constexpr int K = 12, TL = 1 << K, NT = K - 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* tile = reinterpret_cast<A*>(smem_raw);
+  uint64_t* hi_off = reinterpret_cast<uint64_t*>(tile + TL);       // [TL >> lowq]
+  uint32_t* swz = reinterpret_cast<uint32_t*>(hi_off + (TL >> g.lowq));  // [TL >> SB]
+  double* wsum = reinterpret_cast<double*>(swz + (TL >> SB));        // [nterm][8 warps]
+  ExpvalTerm* sterm = reinterpret_cast<ExpvalTerm*>(wsum + (kET / 32) * g.nterm);  // [nterm]
+  EvMap* smap = reinterpret_cast<EvMap*>(sterm + g.nterm);                       // [nmap]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t qmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  const uint64_t lowm = (1ull << g.lowq) - 1;
+  const uint64_t shi = g.smask & ~lowm;
+  for (int h = tid; h < (TL >> g.lowq); h += kET) hi_off[h] = pdep64((uint64_t)h, shi);
+  const uint8_t* V = SB == 3 ? c_swz3 : c_swz4;
+  for (int h = tid; h < (TL >> SB); h += kET) {
+    uint32_t s = 0;
+    for (int p = SB, hh = h; hh; ++p, hh >>= 1)
+      if (hh & 1) s ^= V[p];
+    swz[h] = s;
+  }
+  for (int t = tid; t < g.nterm; t += kET) sterm[t] = terms[g.term_begin + t];
+  for (int m = tid; m < g.nmap; m += kET) smap[m] = maps[g.map_begin + m];
+  __syncthreads();
+  const int ntl = n - K;
+  const int64_t tiles = (int64_t)1 << ntl, W = slots * tiles;
+  const uint64_t outmask = ~g.smask & qmask;
+  // per-thread constant parts of the gather (pdep / swizzle linear over disjoint bits)
+  const uint64_t Pt = ((uint64_t)tid & lowm) | hi_off[tid >> g.lowq];
+  const uint32_t St = swz_slot<SB>(swz, (uint32_t)tid);
+  const int hstep = kET >> g.lowq;
+  for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    const int64_t slot = w >> ntl;
+    const uint64_t base = pdep64((uint64_t)(w & (tiles - 1)), outmask);
+    const A* st = states + (slot << n);
+    {  // next item's runs into L2
+      const int64_t wn = w + gridDim.x;
+      if (wn < W) {
+        const A* sn = states + ((wn >> ntl) << n) + pdep64((uint64_t)(wn & (tiles - 1)), outmask);
+        for (int h = tid; h < (TL >> g.lowq); h += kET) prefetch_line_l2(sn + hi_off[h]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TL / kET; ++i) {  // all 16 loads of a thread in flight at once
+      const A* src = st + (base | Pt | hi_off[i * hstep]);
+      A* dst = tile + (St ^ swz_slot<SB>(swz, (uint32_t)(i * kET)));
+      if (sizeof(A) == 16) cp_async16(dst, src);
+      else cp_async8(dst, src);
+    }
+    cp_async_commit();
+    cp_async_wait0();
+    __syncthreads();
+    for (int mi = 0; mi < g.nmap; ++mi) {
+      const EvMap& m = smap[mi];
+      uint32_t tb = 0;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) tb |= (uint32_t)((tid >> i) & 1) << m.tpos[i];
+      const uint32_t sbase = swz_slot<SB>(swz, tb);
+      A v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = tile[sbase ^ m.soff[j]];
+      for (int t = m.term_begin; t < m.term_begin + m.nterm; ++t) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) opaque(v[j]);
+        const ExpvalTerm& tm = sterm[t - g.term_begin];
+        double acc = ev_term<R>(v, tm.xr, tm.zsig, tm.ny & 1);
+        acc = flip_sign(acc, __popc(tb & tm.zl), 0);
+        for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) wsum[(t - g.term_begin) * (kET / 32) + warp] = acc;
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < g.nterm; t += kET) {  // fixed warp order per term
+      const ExpvalTerm& tm = sterm[t];
+      double s = 0.0;
+      for (int w2 = 0; w2 < kET / 32; ++w2) s += wsum[t * (kET / 32) + w2];
+      if (__popcll(base & tm.zg) & 1) s = -s;
+      partial[w * nterm_total + tm.out] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// partial layout [slot][tile][term]: consecutive threads (terms) read consecutive words
 __global__ void k_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
                                      const ExpvalTerm* terms_by_out, double* out) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= slots * nterm) return;
   const int t = (int)(idx % nterm);
-  const double* p = partial + idx * ((int64_t)1 << ntiles_log2);
+  const int64_t slot = idx / nterm;
+  const int64_t tiles = (int64_t)1 << ntiles_log2;
+  const double* p = partial + slot * tiles * nterm + t;
   double s = 0.0;
-  for (int64_t b = 0; b < ((int64_t)1 << ntiles_log2); ++b) s += p[b];
+  for (int64_t b = 0; b < tiles; ++b) s += p[b * nterm];
   const ExpvalTerm tm = terms_by_out[t];
   if (tm.xg | tm.xl) s *= 2.0;
   out[idx] = ((tm.ny & 3) >= 2) ? -s : s;
@@ -89,10 +248,36 @@ __global__ void k_expval_tile_finish(const double* partial, int64_t slots, int n
 }  // namespace
 
 void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
-                        const ExpvalTerm* terms, double* partial, int nterm_total, cudaStream_t s) {
-  const size_t smem = (size_t)(c64 ? 8 : 16) * ((size_t)1 << g.k) + sizeof(uint64_t) * ((size_t)1 << (g.k - g.lowq)) +
-                      sizeof(double) * (kET / 32) * (size_t)g.nterm;
+                        const ExpvalTerm* terms, const EvMap* maps, double* partial, int nterm_total,
+                        cudaStream_t s) {
   dim3 grid((unsigned)(1ull << (n - g.k)), (unsigned)slots);
+  const size_t amp = c64 ? 8 : 16;
+  if (g.nmap > 0) {
+    const size_t smem = amp * ((size_t)1 << g.k) + sizeof(uint64_t) * ((size_t)1 << (g.k - g.lowq)) +
+                        sizeof(uint32_t) * ((size_t)1 << (g.k - (c64 ? 4 : 3))) +
+                        sizeof(double) * (kET / 32) * (size_t)g.nterm + sizeof(ExpvalTerm) * (size_t)g.nterm +
+                        sizeof(EvMap) * (size_t)g.nmap;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t W = (int64_t)grid.x * slots;
+    if (c64) {
+      cudaFuncSetAttribute(k_expval_reg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expval_reg<float>, kET, smem);
+      const unsigned pg = (unsigned)std::min<int64_t>(W, (int64_t)std::max(1, per_sm) * sms);
+      k_expval_reg<float><<<pg, kET, smem, s>>>((const float2*)states, n, slots, g, terms, maps, partial,
+                                                nterm_total);
+    } else {
+      cudaFuncSetAttribute(k_expval_reg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expval_reg<double>, kET, smem);
+      const unsigned pg = (unsigned)std::min<int64_t>(W, (int64_t)std::max(1, per_sm) * sms);
+      k_expval_reg<double><<<pg, kET, smem, s>>>((const double2*)states, n, slots, g, terms, maps, partial,
+                                                 nterm_total);
+    }
+    return;
+  }
+  const size_t smem = amp * ((size_t)1 << g.k) + sizeof(uint64_t) * ((size_t)1 << (g.k - g.lowq)) +
+                      sizeof(double) * (kET / 32) * (size_t)g.nterm;
   if (c64) {
     cudaFuncSetAttribute(k_expval_tile<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_expval_tile<float><<<grid, kET, smem, s>>>((const float2*)states, n, g, terms, partial, nterm_total);

@@ -39,14 +39,24 @@ struct ExpvalTerm {
   uint32_t xl, zl;  // X|Y and Z|Y letters inside the tile (tile positions)
   uint64_t xg, zg;  // outside the tile (qubit masks; xg must be 0 for the tile path)
   int32_t ny, out;  // #Y, output index
+  uint32_t xr;      // register path: X|Y letters in register-bit space of the term's mapping
+  uint32_t zsig;    // register path: bit j = parity(tile positions of register j & zl)
+};
+// register mapping of a tile group (k = 12): register bit b <-> tile position rpos[b];
+// the terms [term_begin, term_begin + nterm) of the group are evaluated with it
+struct EvMap {
+  int8_t tpos[16];    // thread bit i -> tile position (k - 4 entries)
+  uint16_t soff[16];  // swizzled slot offset of register j
+  int32_t term_begin, nterm;
 };
 struct ExpvalGroup {
   uint64_t smask;   // tile qubits
   int32_t k, lowq, term_begin, nterm;
+  int32_t map_begin, nmap;  // nmap > 0: register-mapped kernel (k == 12)
 };
 void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
-                        const ExpvalTerm* terms, double* partial /*[slots][nterm_total][tiles]*/, int nterm_total,
-                        cudaStream_t s);
+                        const ExpvalTerm* terms, const EvMap* maps,
+                        double* partial /*[slots][tiles][nterm_total]*/, int nterm_total, cudaStream_t s);
 void launch_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
                                const ExpvalTerm* terms_by_out, double* out, cudaStream_t s);
 

@@ -46,6 +46,37 @@ uint32_t swizzle_hi(uint32_t hi, int sb) {
 static uint32_t swz_slot(uint32_t l, int sb) { return l ^ swizzle_hi(l >> sb, sb); }
 static uint32_t swz_vec(int p, int sb) { return p < sb ? (1u << p) : (sb == 3 ? kV3[p] : kV4[p]); }
 
+void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff) {
+  uint32_t R = 0;
+  for (int b = 0; b < rb; ++b) R |= 1u << rpos[b];
+  // thread positions: first sb positions with independent swizzle vectors, so that
+  // 2^sb consecutive threads hit distinct bank groups
+  std::vector<int> tp, others;
+  uint32_t basis[8] = {0};
+  for (int p = 0; p < k; ++p) {
+    if (R >> p & 1) continue;
+    uint32_t v = swz_vec(p, sb);
+    for (int b = sb - 1; b >= 0 && v; --b)
+      if (v >> b & 1) {
+        if (basis[b]) v ^= basis[b];
+        else {
+          basis[b] = v;
+          break;
+        }
+      }
+    if (v && (int)tp.size() < sb) tp.push_back(p);
+    else others.push_back(p);
+  }
+  for (int p : others) tp.push_back(p);
+  for (int i = 0; i < k - rb; ++i) tpos[i] = (int8_t)tp[i];
+  for (int j = 0; j < (1 << rb); ++j) {
+    uint32_t off = 0;
+    for (int b = 0; b < rb; ++b)
+      if (j >> b & 1) off |= 1u << rpos[b];
+    soff[j] = (uint16_t)swz_slot(off, sb);
+  }
+}
+
 static int gate_class_of(int base) {
   switch (base) {
     case QSB_G_X: return GC_XPERM;
@@ -285,31 +316,7 @@ struct Planner {
           rj[p] = nr++;
         }
       }
-      // thread positions: first sb positions with independent swizzle vectors
-      std::vector<int> tp, others;
-      uint32_t basis[8] = {0};
-      for (int p = 0; p < k; ++p) {
-        if (R >> p & 1) continue;
-        uint32_t v = swz_vec(p, sb);
-        for (int b = sb - 1; b >= 0 && v; --b)
-          if (v >> b & 1) {
-            if (basis[b]) v ^= basis[b];
-            else {
-              basis[b] = v;
-              break;
-            }
-          }
-        if (v && (int)tp.size() < sb) tp.push_back(p);
-        else others.push_back(p);
-      }
-      for (int p : others) tp.push_back(p);
-      for (int i = 0; i < nt; ++i) ph.tpos[i] = (int8_t)tp[i];
-      for (int j = 0; j < (1 << rb); ++j) {
-        uint32_t off = 0;
-        for (int b = 0; b < rb; ++b)
-          if (j >> b & 1) off |= 1u << rpos[b];
-        ph.soff[j] = (uint16_t)swz_slot(off, sb);
-      }
+      tile_mapping(rpos, rb, k, sb, ph.tpos, ph.soff);
       ph.gate_begin = (int)P.phase_gates.size();
       for (int gi : take) {
         const PassGate& g = P.gates[gi];

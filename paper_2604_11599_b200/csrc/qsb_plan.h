@@ -31,6 +31,10 @@ struct Step {
 // V linear; `sb` = 3 for 16-byte amplitudes, 4 for 8-byte ones.
 int swizzle_bits(int c64);
 uint32_t swizzle_hi(uint32_t hi, int sb);  // V applied to tile bits >= sb (hi = l >> sb)
+// register / thread mapping of a swizzled k-position tile: register bit b <-> tile
+// position rpos[b] (b < rb); writes the k - rb thread positions and the swizzled slot
+// offset of each of the 2^rb registers
+void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff);
 
 struct StreamPlan {
   int k = 0, lowq = 0, ntiles_log2 = 0, rb = 0;

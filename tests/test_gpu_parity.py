@@ -382,3 +382,21 @@ def test_device_histogram_matches_per_shot_words(golden, prec):
         b = ir.bind(ir.kernel_from_json(case["kernel"]), [])
         if prec == "c128":
             assert sim.sample(b, 1024, 1234).counts == case["hist_1024_seed1234"], name
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_observe_register_mapped_reducer(prec):
+    """Full 12-qubit tiles take the register-mapped Pauli kernel: X supports up to 5
+    letters (> 4 forces extra mappings / groups), Y phases, out-of-tile Z signs and
+    diagonal terms, per term against the oracle's expval_pauli."""
+    n = 15
+    k = workloads.random_static(n, 200, seed=61, nparams=3, max_controls=1)
+    vals = [0.2, -1.3, 0.8]
+    ham = workloads.vqe_hamiltonian(n=n, terms=70, seed=5)
+    ham += [(0.5, "X" * 5 + "I" * (n - 5)), (-0.25, "I" * 3 + "YZXZY" + "I" * (n - 8)),
+            (0.75, "Z" * n), (0.1, "I" * n), (0.3, "Y" + "I" * (n - 2) + "X")]
+    e, terms = sim.observe(k, ham, [vals], precision=prec, return_terms=True)
+    st = P.final_state(ir.bind(k, vals))
+    want = np.array([P.pauli_expectation(st, w) for _, w in ham])
+    assert np.max(np.abs(terms[0] - want)) <= 4 * TOL[prec]
+    assert abs(e[0] - sum(c * v for (c, _), v in zip(ham, want))) <= TOL[prec] * sum(abs(c) for c, _ in ham)
