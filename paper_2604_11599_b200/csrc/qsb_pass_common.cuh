@@ -273,7 +273,9 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
         double* out = a.partial + it.slot * a.partial_stride + (int64_t)t_log * nb;
         if (nb <= T) {
           const int tp = T / nb;
-          const int bb = tid / tp, j = tid % tp;
+          // bin fastest across the warp: neighbouring threads read neighbouring
+          // amplitudes when the measured qubits are low tile positions (the common case)
+          const int bb = tid % nb, j = tid / nb;
           uint32_t bpos = 0;
           for (int jj = 0; jj < ml; ++jj)
             if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
@@ -282,15 +284,30 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
           // (x | ~mask) + d carries across the holes), in increasing order
           const uint32_t inc = (uint32_t)pdep64((uint64_t)tp, free_mask);
           uint32_t f = (uint32_t)pdep64((uint64_t)j, free_mask);
-          for (int r = j; r < members; r += tp) {
-            s += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
-            f = ((f | ~free_mask) + inc) & free_mask;
+          auto step = [&](uint32_t x) { return ((x | ~free_mask) + inc) & free_mask; };
+          // four independent accumulators (fixed association): the shared loads and
+          // FP64 adds of consecutive members overlap instead of forming one chain
+          const int cnt = (members - j + tp - 1) / tp;
+          double s4[4] = {0.0, 0.0, 0.0, 0.0};
+          int i = 0;
+          for (; i + 4 <= cnt; i += 4) {
+            const uint32_t f1 = step(f), f2 = step(f1), f3 = step(f2);
+            s4[0] += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+            s4[1] += norm2<R>(tile[swz_slot<SB>(swz, f1 | bpos)]);
+            s4[2] += norm2<R>(tile[swz_slot<SB>(swz, f2 | bpos)]);
+            s4[3] += norm2<R>(tile[swz_slot<SB>(swz, f3 | bpos)]);
+            f = step(f3);
           }
+          for (; i < cnt; ++i) {
+            s4[0] += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+            f = step(f);
+          }
+          s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
           red[tid] = s;
           __syncthreads();
           if (j == 0) {
             double tot = 0.0;
-            for (int jj = 0; jj < tp; ++jj) tot += red[bb * tp + jj];
+            for (int jj = 0; jj < tp; ++jj) tot += red[bb + nb * jj];
             out[bb] = tot;
           }
         } else {
