@@ -52,25 +52,63 @@ struct PassItem {
   double sre, sim;
 };
 
-__device__ __forceinline__ PassItem pass_item(const StreamArgs& a, const PassDesc& pd, int64_t w, int ntl) {
+// Per-CTA nibble tables for the per-item bit scatters / gathers (all linear over
+// disjoint bit fields, so a 64-bit operand is the OR of one entry per 4-bit chunk):
+//   pdt[c][v]: pdep of (v << 4c) into the out-of-tile qubits   (tile id -> base)
+//   pxs[c][v]: tile positions of the qubits of (v << 4c)        (frame -> tile flip)
+//   pxo[c][v]: pext of (v << 4c) over the out-of-tile qubits    (frame -> tile id flip)
+struct ItemTables {
+  uint64_t* pdt;
+  uint32_t* pxs;
+  uint64_t* pxo;
+};
+constexpr int kItemChunks = 16;  // 64 bits / 4
+__host__ __device__ inline size_t item_tables_bytes() {
+  return (2 * sizeof(uint64_t) + sizeof(uint32_t)) * kItemChunks * 16;
+}
+
+__device__ __forceinline__ void build_item_tables(const ItemTables& tb, const PassDesc& pd, int n, int tid, int T) {
+  const uint64_t qmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  const uint64_t out = ~pd.smask & qmask;
+  for (int e = tid; e < kItemChunks * 16; e += T) {
+    const int c = e >> 4;
+    const uint64_t v = (uint64_t)(e & 15) << (4 * c);
+    tb.pdt[e] = pdep64(v, out);
+    tb.pxo[e] = pext64(v & out, out);
+    uint32_t f = 0;
+    for (int j = 0; j < pd.k; ++j)
+      if ((v >> pd.sq[j]) & 1) f |= 1u << j;
+    tb.pxs[e] = f;
+  }
+}
+
+__device__ __forceinline__ uint64_t tab64(const uint64_t* t, uint64_t x, int nbits) {
+  uint64_t r = 0;
+  for (int c = 0; c * 4 < nbits; ++c) r |= t[c * 16 + ((x >> (4 * c)) & 15)];
+  return r;
+}
+__device__ __forceinline__ uint32_t tab32(const uint32_t* t, uint64_t x, int nbits) {
+  uint32_t r = 0;
+  for (int c = 0; c * 4 < nbits; ++c) r |= t[c * 16 + ((x >> (4 * c)) & 15)];
+  return r;
+}
+
+__device__ __forceinline__ PassItem pass_item(const StreamArgs& a, const PassDesc& pd, int64_t w, int ntl,
+                                              const ItemTables& tb) {
   PassItem it;
   it.slot = a.active ? a.active[w >> ntl] : (w >> ntl);  // representative slots only (history dedup)
   const uint64_t tile = (uint64_t)w & ((1ull << ntl) - 1);
   const TrajCtl* c = a.ctl + it.slot;
   it.alive = c->status == 0;
-  const uint64_t qmask = (a.n >= 64) ? ~0ull : ((1ull << a.n) - 1);
   const uint64_t F = c->frame & ~pd.clear_before;
   it.pending = pd.prologue && c->pending;
   it.Kp = c->kmask;
   it.Vp = c->kval;
   it.sre = c->sre;
   it.sim = c->sim;
-  it.base_phys = pdep64(tile, ~pd.smask & qmask);
+  it.base_phys = tab64(tb.pdt, tile, ntl);
   it.base_log = it.base_phys ^ (F & ~pd.smask);
-  uint32_t fl = 0;
-  for (int j = 0; j < pd.k; ++j)
-    if ((F >> pd.sq[j]) & 1) fl |= 1u << j;
-  it.fl = fl;
+  it.fl = tab32(tb.pxs, F, a.n);
   return it;
 }
 
@@ -99,7 +137,8 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
   const size_t amp = c64 ? 8 : 16;
   const size_t sgate = c64 ? 64 : 96;
   return pass_buffers(c64) * (amp << pd.k) + sgate * pd.pgate_count + (sizeof(uint64_t) << (pd.k - pd.lowq)) +
-         (sizeof(uint32_t) << (pd.k - sb)) + sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb);
+         (sizeof(uint32_t) << (pd.k - sb)) + sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) +
+         item_tables_bytes() + 16;
 }
 
 __device__ __forceinline__ void prefetch_line_l2(const void* gmem) {
@@ -119,6 +158,11 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   uint32_t* swz = reinterpret_cast<uint32_t*>(hi_off + (TL >> pd.lowq));
   double* red = reinterpret_cast<double*>(swz + (TL >> SB));
   uint32_t* ujt = reinterpret_cast<uint32_t*>(red + T);  // [2^RB] swizzled slot of j*T
+  ItemTables itb;
+  itb.pdt = reinterpret_cast<uint64_t*>((reinterpret_cast<size_t>(ujt + (1 << RB)) + 15) & ~(size_t)15);
+  itb.pxo = itb.pdt + kItemChunks * 16;
+  itb.pxs = reinterpret_cast<uint32_t*>(itb.pxo + kItemChunks * 16);
+  build_item_tables(itb, pd, a.n, tid, T);
   const uint64_t lowm = (1ull << pd.lowq) - 1;
   const uint64_t shi = pd.smask & ~lowm;
   for (int h = tid; h < (TL >> pd.lowq); h += T) hi_off[h] = pdep64((uint64_t)h, shi);
@@ -184,7 +228,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   int64_t w = blockIdx.x;
   PassItem cur;
   cur.alive = false;
-  if (w < W) cur = pass_item(a, pd, w, ntl);
+  if (w < W) cur = pass_item(a, pd, w, ntl, itb);
   if (NB == 2 && w < W) prefetch(cur, bufs);
   cp_async_commit();
   int b = 0;
@@ -192,7 +236,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     const int64_t wn = w + gridDim.x;
     PassItem nxt;
     nxt.alive = false;
-    if (wn < W) nxt = pass_item(a, pd, wn, ntl);
+    if (wn < W) nxt = pass_item(a, pd, wn, ntl, itb);
     if (NB == 2) {
       if (wn < W) prefetch(nxt, bufs + (b ^ 1) * TL);
       cp_async_commit();
@@ -269,7 +313,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
         for (int j = 0; j < ml; ++j) mlm |= 1u << pd.mloc[j];
         const uint32_t free_mask = ((uint32_t)TL - 1) & ~mlm;
         const int members = TL >> ml;
-        const uint64_t t_log = pext64(it.base_log, ~pd.smask & qmask);
+        const uint64_t t_log = tab64(itb.pxo, it.base_log, a.n);
         double* out = a.partial + it.slot * a.partial_stride + (int64_t)t_log * nb;
         if (nb <= T) {
           const int tp = T / nb;
