@@ -33,6 +33,10 @@ namespace {
 
 constexpr int kET = 256;
 
+__device__ __forceinline__ void prefetch_line_l2(const void* gmem) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gmem));
+}
+
 // ---- pair-loop kernel (any tile size) -------------------------------------------
 
 template <typename R>

@@ -126,9 +126,9 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 
 // Buffering mode: complex64 tiles (32 KiB) double-buffer in shared memory (two CTAs per
 // SM still fit); complex128 tiles (64 KiB) keep one buffer so that two CTAs share an SM,
-// and the next item is prefetched into L2 (one prefetch.global.L2 per 128-byte line,
-// issued per thread: the bulk TMA prefetch takes a warp-uniform address and compiled
-// to a 32-iteration loop per warp) while the current one computes, so its gather hits L2.
+// and the two CTAs' gather / compute / scatter phases overlap each other.  (Measured:
+// an L2 prefetch of the next item -- bulk or per line -- and one double-buffered CTA
+// per SM were both slower.)
 __host__ __device__ inline int pass_buffers(int c64) { return c64 ? 2 : 1; }
 
 // dynamic shared memory of a register-blocked pass
@@ -141,9 +141,6 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
          item_tables_bytes() + 16;
 }
 
-__device__ __forceinline__ void prefetch_line_l2(const void* gmem) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gmem));
-}
 
 template <typename R, int RB, typename PhaseRunner>
 __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassDesc& pd, unsigned char* smem_raw,
@@ -215,15 +212,6 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     }
   };
 
-  auto prefetch_next_l2 = [&](const PassItem& it) {  // the 128-byte lines of one 2^lowq run per thread
-    if (!it.alive || pd.init_zero) return;
-    const char* st = reinterpret_cast<const char*>(reinterpret_cast<const A*>(a.state) + (it.slot << a.n));
-    const unsigned run = (unsigned)(sizeof(A) << pd.lowq);
-    for (int h = tid; h < (TL >> pd.lowq); h += T) {
-      const char* r0 = st + sizeof(A) * (it.base_phys | hi_off[h]);
-      for (unsigned o = 0; o < run; o += 128) prefetch_line_l2(r0 + o);
-    }
-  };
 
   int64_t w = blockIdx.x;
   PassItem cur;
@@ -242,7 +230,6 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
       cp_async_commit();
       cp_async_wait1();
     } else {
-      if (wn < W) prefetch_next_l2(nxt);
       prefetch(cur, bufs);
       cp_async_commit();
       cp_async_wait0();
