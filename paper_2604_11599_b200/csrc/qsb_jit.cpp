@@ -323,7 +323,17 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pd.k - P.rb)) << ", " << (mb && *mb ? atoi(mb) : 2)
     << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-  o << "  qsb::pass_persistent<R, " << P.rb << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
+  // staging is needed only if a phase reads the staged gates: per-item skips (guards,
+  // out-of-tile controls, per-tile diagonal factors), non-literal matrices, swap phases
+  bool stage = false;
+  for (int g = pd.pgate_begin; g < pd.pgate_begin + pd.pgate_count; ++g) {
+    const PhaseGate& q = P.phase_gates[g];
+    if (q.guard >= 0 || q.gcm != 0 || q.kind == PK_DIAG_G || !t.mats[q.mat].has_matrix) stage = true;
+  }
+  for (int i = 0; i < pd.phase_count; ++i)
+    if (P.phases[pd.phase_begin + i].nt < 0) stage = true;
+  o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false")
+    << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) o << "    ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";

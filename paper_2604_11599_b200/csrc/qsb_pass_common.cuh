@@ -142,7 +142,12 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
 }
 
 
-template <typename R, int RB, typename PhaseRunner>
+// STAGE: stage the pass gates into shared memory per item (guards, out-of-tile
+// controls, per-tile diagonal factors, per-point matrices).  The NVRTC kernels pass
+// false when none of their phases reads the staged gates (literal matrices from the
+// constant bank, no per-item decisions), which removes a global-load round trip and a
+// barrier from every item.
+template <typename R, int RB, bool STAGE = true, typename PhaseRunner>
 __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassDesc& pd, unsigned char* smem_raw,
                                                 PhaseRunner run) {
   using A = typename Amp<R>::T;
@@ -252,7 +257,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
           *d = v;
         }
       }
-      {  // stage the gates: guards, out-of-tile controls, per-CTA diagonal factors
+      if (STAGE) {  // stage the gates: guards, out-of-tile controls, per-CTA diagonal factors
         const uint32_t* gw = a.guards + it.slot * a.gwords;
         const double* mats = a.mats + it.slot * a.mat_stride;
         for (int i = tid; i < pd.pgate_count; i += T) {
@@ -290,7 +295,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
           sg[i] = s;
         }
       }
-      __syncthreads();
+      if (STAGE || it.pending) __syncthreads();
       PassCtx<R> cx{tile, sg, swz, tid, T, TL};
       run(cx);  // the phases (each ends with __syncthreads)
       if (pd.epi) {  // per-tile marginal of the next region's measured qubits (fixed order)
