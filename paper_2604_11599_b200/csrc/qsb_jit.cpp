@@ -281,6 +281,19 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
 
 bool jit_available() { return nvrtc().ok; }
 
+// staging is needed only if a phase reads the staged gates: per-item skips (guards,
+// out-of-tile controls, per-tile diagonal factors), non-literal matrices, swap phases
+bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass) {
+  const PassDesc& pd = P.passes[pass];
+  for (int g = pd.pgate_begin; g < pd.pgate_begin + pd.pgate_count; ++g) {
+    const PhaseGate& q = P.phase_gates[g];
+    if (q.guard >= 0 || q.gcm != 0 || q.kind == PK_DIAG_G || !t.mats[q.mat].has_matrix) return true;
+  }
+  for (int i = 0; i < pd.phase_count; ++i)
+    if (P.phases[pd.phase_begin + i].nt < 0) return true;
+  return false;
+}
+
 std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
   const PassDesc& pd = P.passes[pass];
   const int sb = c64 ? 4 : 3;
@@ -323,15 +336,7 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pd.k - P.rb)) << ", " << (mb && *mb ? atoi(mb) : 2)
     << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-  // staging is needed only if a phase reads the staged gates: per-item skips (guards,
-  // out-of-tile controls, per-tile diagonal factors), non-literal matrices, swap phases
-  bool stage = false;
-  for (int g = pd.pgate_begin; g < pd.pgate_begin + pd.pgate_count; ++g) {
-    const PhaseGate& q = P.phase_gates[g];
-    if (q.guard >= 0 || q.gcm != 0 || q.kind == PK_DIAG_G || !t.mats[q.mat].has_matrix) stage = true;
-  }
-  for (int i = 0; i < pd.phase_count; ++i)
-    if (P.phases[pd.phase_begin + i].nt < 0) stage = true;
+  const bool stage = pass_needs_stage(t, P, pass);
   o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false")
     << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
   for (int i = 0; i < pd.phase_count; ++i) {
@@ -417,7 +422,7 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vect
     JitKernel& jk = out[j.pass];
     jk.lib = (void*)lib;
     jk.kern = (void*)k;
-    jk.smem = pass_reg_smem(c64, P.passes[j.pass], P.rb);
+    jk.smem = pass_reg_smem(c64, P.passes[j.pass], P.rb, t.n, pass_needs_stage(t, P, j.pass));
     jk.threads = 1 << (P.passes[j.pass].k - P.rb);
     e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
     if (e != cudaSuccess) {

@@ -21,6 +21,9 @@ struct JitKernel {
 // true if libnvrtc could be loaded
 bool jit_available();
 
+// true if a phase of the pass reads the per-item staged gates (see pass_persistent)
+bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass);
+
 // Generates, compiles (parallel, cached by source hash in $QSB_JIT_CACHE or
 // /tmp/qsb_jit_cache) and loads one kernel per register-blocked pass of `P`.
 // out[i] stays empty for passes without phases.  Returns "" or an error.

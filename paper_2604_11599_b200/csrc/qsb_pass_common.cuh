@@ -62,15 +62,15 @@ struct ItemTables {
   uint32_t* pxs;
   uint64_t* pxo;
 };
-constexpr int kItemChunks = 16;  // 64 bits / 4
-__host__ __device__ inline size_t item_tables_bytes() {
-  return (2 * sizeof(uint64_t) + sizeof(uint32_t)) * kItemChunks * 16;
+__host__ __device__ inline int item_chunks(int n) { return (n + 3) / 4; }  // 4-bit chunks of a qubit mask
+__host__ __device__ inline size_t item_tables_bytes(int n) {
+  return (2 * sizeof(uint64_t) + sizeof(uint32_t)) * item_chunks(n) * 16;
 }
 
 __device__ __forceinline__ void build_item_tables(const ItemTables& tb, const PassDesc& pd, int n, int tid, int T) {
   const uint64_t qmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
   const uint64_t out = ~pd.smask & qmask;
-  for (int e = tid; e < kItemChunks * 16; e += T) {
+  for (int e = tid; e < item_chunks(n) * 16; e += T) {
     const int c = e >> 4;
     const uint64_t v = (uint64_t)(e & 15) << (4 * c);
     tb.pdt[e] = pdep64(v, out);
@@ -132,13 +132,13 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 __host__ __device__ inline int pass_buffers(int c64) { return c64 ? 2 : 1; }
 
 // dynamic shared memory of a register-blocked pass
-__host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int rb) {
+__host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int rb, int n, bool stage) {
   const int sb = c64 ? 4 : 3;
   const size_t amp = c64 ? 8 : 16;
   const size_t sgate = c64 ? 64 : 96;
-  return pass_buffers(c64) * (amp << pd.k) + sgate * pd.pgate_count + (sizeof(uint64_t) << (pd.k - pd.lowq)) +
-         (sizeof(uint32_t) << (pd.k - sb)) + sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) +
-         item_tables_bytes() + 16;
+  return pass_buffers(c64) * (amp << pd.k) + (stage ? sgate * pd.pgate_count : 0) +
+         (sizeof(uint64_t) << (pd.k - pd.lowq)) + (sizeof(uint32_t) << (pd.k - sb)) +
+         sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) + item_tables_bytes(n) + 16;
 }
 
 
@@ -156,14 +156,14 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   constexpr int NB = sizeof(R) == 4 ? 2 : 1;  // pass_buffers()
   A* bufs = reinterpret_cast<A*>(smem_raw);
   SGate<R>* sg = reinterpret_cast<SGate<R>*>(bufs + NB * TL);
-  uint64_t* hi_off = reinterpret_cast<uint64_t*>(sg + pd.pgate_count);
+  uint64_t* hi_off = reinterpret_cast<uint64_t*>(sg + (STAGE ? pd.pgate_count : 0));
   uint32_t* swz = reinterpret_cast<uint32_t*>(hi_off + (TL >> pd.lowq));
   double* red = reinterpret_cast<double*>(swz + (TL >> SB));
   uint32_t* ujt = reinterpret_cast<uint32_t*>(red + T);  // [2^RB] swizzled slot of j*T
   ItemTables itb;
   itb.pdt = reinterpret_cast<uint64_t*>((reinterpret_cast<size_t>(ujt + (1 << RB)) + 15) & ~(size_t)15);
-  itb.pxo = itb.pdt + kItemChunks * 16;
-  itb.pxs = reinterpret_cast<uint32_t*>(itb.pxo + kItemChunks * 16);
+  itb.pxo = itb.pdt + item_chunks(a.n) * 16;
+  itb.pxs = reinterpret_cast<uint32_t*>(itb.pxo + item_chunks(a.n) * 16);
   build_item_tables(itb, pd, a.n, tid, T);
   const uint64_t lowm = (1ull << pd.lowq) - 1;
   const uint64_t shi = pd.smask & ~lowm;

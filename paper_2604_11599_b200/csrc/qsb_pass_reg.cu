@@ -155,7 +155,7 @@ int num_sms() {
 
 template <typename R, int RB> cudaError_t launch_t(const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
   const int T = 1 << (pd.k - RB);
-  const size_t sm = pass_reg_smem(a.c64, pd, RB);
+  const size_t sm = pass_reg_smem(a.c64, pd, RB, a.n, true);
   cudaError_t e = cudaFuncSetAttribute(k_pass_reg<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
