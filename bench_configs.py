@@ -112,6 +112,18 @@ def cfg5(args):
     dt = time.perf_counter() - t0
     _emit({"config": f"cfg5 sliced RDC{n} depth 40, 3 global qubits emulated on 1 GPU (8 slices)",
            "trajectory_s": dt, "exchanges": st.exchanges, "key": store.key()})
+    # the same at a slice size where the fused slice passes pay: RDC30 over 8 slices
+    _, k = workloads.rdc_circuit(n=30, depth=20, every=10, seed=34)
+    b = ir.bind(k, [])
+    for fuse in (False, True):
+        t0 = time.perf_counter()
+        store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(1234, 0), 3,
+                                                 backend=sliced.GpuSliceBackend(fuse=fuse))
+        dt = time.perf_counter() - t0
+        _emit({"config": f"cfg5 sliced RDC30 depth 20, 3 global qubits emulated (8 slices of 2^27), "
+                         f"{'fused' if fuse else 'per-op'} slice gates",
+               "trajectory_s": dt, "exchanges": st.exchanges, "key": store.key()})
+        del st
 
 
 def cfg5_single(args):

@@ -180,6 +180,12 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
 /* statevector (sim.py:402-409): static tapes only (QSB_ERR_DYNAMIC otherwise).       */
 int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out);
 
+/* apply a gates-only tape to a state IN PLACE (the fused streaming passes of
+ * qsb_statevector without the |0...0> start): the sequence of apply_gate calls
+ * (sim.py:224-227) it replaces, fused.  Used by the sliced executor to run the local
+ * gates between two exchanges on each slice in a few passes.                         */
+int32_t qsb_apply_tape(qsb_tape tp, const double* params, qsb_state st);
+
 /* _sample_static (sim.py:354-369): one simulation, sequential fp64 cumsum, per-shot
  * searchsorted(side="right"), top-level measures written in program order.           */
 int32_t qsb_sample_static(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,

@@ -103,6 +103,7 @@ _SIGS = {
     "qsb_run_trajectory": (_I32, [_P, _I32, _P, _P, _U64, _I64, _P, _I32, _P, _P, _P, _I32, ctypes.POINTER(_I32),
                                   ctypes.POINTER(_I32)]),
     "qsb_statevector": (_I32, [_P, _P, _P]),
+    "qsb_apply_tape": (_I32, [_P, _P, _P]),
     "qsb_sample_static": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P]),
     "qsb_sample_counts": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P, _P, _I64, ctypes.POINTER(_I64)]),
     "qsb_observe": (_I32, [_P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P, _P]),

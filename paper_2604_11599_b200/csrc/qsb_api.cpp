@@ -269,6 +269,7 @@ struct StreamRun {
   double pass_bytes = 0;
   int64_t passes = 0, decides = 0, launches = 0;
   std::vector<std::pair<int, int>> pass_event_idx;
+  bool in_place = false;  // apply to the state already in `state` (no |0...0> initialisation)
 };
 
 int alloc_stream_scratch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, int64_t slots) {
@@ -331,7 +332,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   }
   r.physical_counted = dedup;
   if (dedup) ctx->run_physical = true;
-  if (P.passes.empty()) {
+  if (P.passes.empty() && !r.in_place) {
     launch_init_zero(r.c64, r.state, t.n, r.slots, ctx->stream);
     r.launches++;
   }
@@ -346,7 +347,8 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   const double state_bytes = (double)amp_bytes(r.c64) * (double)((int64_t)1 << t.n) * (double)r.slots;
   for (const Step& s : P.steps) {
     if (s.type == 0) {
-      const PassDesc& pd = P.passes[s.index];
+      PassDesc pd = P.passes[s.index];
+      if (r.in_place) pd.init_zero = 0;
       cudaEventRecord(ctx->pass_events[2 * s.index], ctx->stream);
       if (s.index < (int)r.pd->jit.size() && r.pd->jit[s.index].kern)
         QSB_CUDA(jit_launch(r.pd->jit[s.index], a, pd, ctx->stream));
@@ -1246,6 +1248,40 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
   if (status == QSB_ERR_DEGENERATE) return fail(status, "selected measurement branch has probability < 1e-15");
   if (status == QSB_ERR_PREDRAWN) return fail(status, "pre-drawn uniform stream exhausted");
   if (status != QSB_OK) return fail(status, "trajectory failed");
+  return QSB_OK;
+}
+
+int32_t qsb_apply_tape(qsb_tape tp, const double* params, qsb_state st) {
+  const TapeInfo& t = tp->info;
+  if (t.top_level_dynamic) return fail(QSB_ERR_DYNAMIC, "apply_tape needs a gates-only tape");
+  if (st->n != t.n) return fail(QSB_ERR_DIMENSION, "state has the wrong qubit count");
+  qsb_ctx ctx = tp->ctx;
+  DeviceGuard g(ctx->device);
+  const int c64 = st->c64;
+  QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 32, ctx->stream));
+  ctx->run_flops = 0;
+  ctx->run_physical = false;
+  RunTimer timer(ctx);
+  const double* d_params = nullptr;
+  int rc = upload_params(tp, params, 1, &d_params);
+  if (rc) return rc;
+  const double* mats;
+  int64_t mstride;
+  rc = prepare_mats(tp, d_params, 1, &mats, &mstride);
+  if (rc) return rc;
+  PlanDev* pd;
+  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  if (rc) return rc;
+  StreamRun r{tp, pd, c64, 1, st->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
+  r.in_place = true;
+  rc = run_stream(ctx, r);
+  if (rc) return rc;
+  float ms = timer.stop();
+  rc = check_sticky();
+  if (rc) return rc;
+  finish_stats(ctx, ms, pass_ms_sum(ctx, pd->plan.passes.size()), r.pass_bytes, r.passes, r.decides, r.launches, 1,
+               pd->plan.k);
+  note_jit(ctx, pd);
   return QSB_OK;
 }
 

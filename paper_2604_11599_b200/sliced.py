@@ -24,12 +24,13 @@ Operations (reference semantics: sim.py:203-259, 279-314):
 
 The slice backend (device kernels) and the transport (exchange / all-gather) are
 injected; `GpuSliceBackend` + `LocalTransport` / `DistTransport` are the product
-paths.  Gate application on slices is per-op in this round (fusion of sliced passes
-is the next step).
+paths.  Local gates between two exchanges / measurements run as one fused tape per
+slice (`GpuSliceBackend.flush`, C ABI `qsb_apply_tape`).
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -53,11 +54,25 @@ class _G:  # minimal Gate stand-in for local application
 
 
 class GpuSliceBackend:
-    """Slices are device StateVectors on one GPU; kernels through the C ABI."""
+    """Slices are device StateVectors on one GPU; kernels through the C ABI.
 
-    def __init__(self, precision=None, device=None):
+    Local gates are queued per slice and run as ONE fused tape (`qsb_apply_tape`: the
+    streaming engine's register-blocked passes, in place) when the slice is next
+    needed for anything else -- an exchange, a probability, a collapse, a scale or a
+    read -- so the gates between two exchanges cost a few state passes instead of one
+    pass each.  The fused tapes use the generic kernel (no per-tape NVRTC compile).
+    Small slices (the 1-GPU emulations) stay per-op: building a tape costs more than
+    a pass over them."""
+
+    # below this many local qubits a slice pass is cheaper than building a fused tape
+    # (tape + plan construction costs ~ms on the host)
+    FUSE_MIN_LOCAL = 24
+
+    def __init__(self, precision=None, device=None, fuse: bool | None = None):
         self.precision = precision
         self.device = device
+        self.fuse = fuse  # None: fuse slices of >= FUSE_MIN_LOCAL qubits
+        self._queue: dict = {}  # id(slice) -> (slice, [qsb_op records])
 
     def new_slice(self, L: int, initial_one: bool):
         from . import sim
@@ -67,8 +82,31 @@ class GpuSliceBackend:
             self.scale(st, 0.0)
         return st
 
+    def flush(self, st=None) -> None:
+        """Run the queued gates of `st` (or of every slice) as one fused tape."""
+        from . import _lib
+
+        keys = [id(st)] if st is not None else list(self._queue)
+        for key in keys:
+            item = self._queue.pop(key, None)
+            if item is None:
+                continue
+            sl, recs = item
+            ops = np.concatenate(recs)
+            ctx = sl._ctx
+            tape = ctypes.c_void_p()
+            ctx.set_option("jit", 0)
+            try:
+                _lib.check(ctx.lib.qsb_tape_create(ctx.handle, _lib.ptr(ops), len(ops), sl.n, 0, 0, ctypes.byref(tape)))
+                try:
+                    _lib.check(ctx.lib.qsb_apply_tape(tape, None, sl._device()))
+                finally:
+                    ctx.lib.qsb_tape_destroy(tape)
+            finally:
+                ctx.set_option("jit", 1)
+
     def apply(self, st, base, matrix, target, ctrl_local):
-        from . import _lib, sim
+        from . import _lib
 
         rec = np.zeros(1, dtype=_lib.OP_DTYPE)
         r = rec[0]
@@ -85,19 +123,22 @@ class GpuSliceBackend:
         rec["mat"][0][:] = [matrix[0, 0].real, matrix[0, 0].imag, matrix[0, 1].real, matrix[0, 1].imag,
                             matrix[1, 0].real, matrix[1, 0].imag, matrix[1, 1].real, matrix[1, 1].imag]
         rec["has_matrix"] = 1
+        if self.fuse or (self.fuse is None and st.n >= self.FUSE_MIN_LOCAL):
+            self._queue.setdefault(id(st), (st, []))[1].append(rec)
+            return
         _lib.check(st._ctx.lib.qsb_apply_gate(st._device(), _lib.ptr(rec), None, 0))
 
     def scale(self, st, c: complex):
         from . import _lib
 
+        self.flush(st)
         c = complex(c)
         _lib.check(st._ctx.lib.qsb_state_scale(st._device(), c.real, c.imag))
 
     def prob1(self, st, q: int) -> float:
-        import ctypes
-
         from . import _lib
 
+        self.flush(st)
         out = ctypes.c_double()
         _lib.check(st._ctx.lib.qsb_state_prob1(st._device(), int(q), ctypes.byref(out)))
         return float(out.value)
@@ -105,16 +146,16 @@ class GpuSliceBackend:
     def collapse(self, st, q, outcome, scale, flip):
         from . import _lib
 
+        self.flush(st)
         _lib.check(st._ctx.lib.qsb_state_collapse(st._device(), int(q), int(outcome), float(scale), int(flip)))
 
     def view(self, st):
         """Zero-copy torch view (float64 / float32 pairs) of the slice's device buffer."""
-        import ctypes
-
         import torch
 
         from . import _lib
 
+        self.flush(st)
         ptr = ctypes.c_void_p()
         _lib.check(st._ctx.lib.qsb_state_device_ptr(st._device(), ctypes.byref(ptr)))
         st._ctx.synchronize()
@@ -132,6 +173,7 @@ class GpuSliceBackend:
         torch.cuda.synchronize(st._ctx.device)
 
     def to_numpy(self, st) -> np.ndarray:
+        self.flush(st)
         return st.amps.copy()
 
 
@@ -271,7 +313,8 @@ class SlicedState:
             else:  # phase on the first local control, the rest stay controls
                 (c, pol), rest = local[0], local[1:]
                 dm = np.array([[1, 0], [0, d]] if pol else [[d, 0], [0, 1]], dtype=np.complex128)
-                self.backend.apply(st, "p", dm, c, rest)
+                # a general diagonal ("rz" class): with pol = 0 the |0> entry is not 1
+                self.backend.apply(st, "rz", dm, c, rest)
 
     def _p1(self, q: int) -> float:
         p = self.perm[q]
@@ -346,4 +389,6 @@ def run_trajectory_sliced(bound, rng, global_qubits: int, *, backend=None, trans
                 run(op.then_body if taken else op.else_body)
 
     run(k.body)
+    if hasattr(backend, "flush"):
+        backend.flush()
     return store, st
