@@ -224,6 +224,12 @@ int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqubits, int32
 int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
                          int32_t precision, int32_t reg_bits, double* out);
 
+/* host-only: register-phase gate fusion of the NVRTC kernels (qsb_plan.h fuse_phase) over
+ * a tape's streaming plan (tile 12).  out[0..5] = {phases, fused blocks, gates folded into
+ * blocks, host-check failures, pass flops per state unfused, the same fused}.          */
+int32_t qsb_fusion_stats(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                         int32_t precision, int32_t reg_bits, double* out);
+
 /* debug / known-answer hook: the first `count` uniforms of RngStream.for_shot(seed, shot)
  * drawn by the DEVICE generator (pins the on-device RNG to sim.py:54-72).              */
 int32_t qsb_debug_rng(qsb_ctx ctx, uint64_t seed, int64_t shot, int32_t count, double* out);

@@ -74,7 +74,7 @@ struct qsb_ctx_s {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<cudaEvent_t> pass_events;
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
-  int64_t opt_dedup = 1, opt_reg_bits = 4;
+  int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1;
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
   DevBuf shotwords, histo;  // device-side shot histogram (qsb_sample_counts)
   qsb_stats last{};
@@ -153,7 +153,8 @@ int reg_bits(qsb_ctx ctx) { return (int)ctx->opt_reg_bits; }  // amplitudes per 
 int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
   const int c64 = lowq == 5 ? 1 : 0;
   const bool want_jit = tp->ctx->opt_jit && tp->info.n >= tp->ctx->opt_jit_min;
-  int key = ((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0);
+  const bool fuse = tp->ctx->opt_fuse != 0;
+  int key = (((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0)) * 2 + (fuse ? 1 : 0);
   auto it = tp->plans.find(key);
   if (it != tp->plans.end()) {
     *out = it->second.get();
@@ -183,9 +184,12 @@ int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
   for (size_t i = 0; i < P.passes.size(); ++i)
     if (P.passes[i].phase_count) pd->pflops[i] = pass_flops(tp->info, P, (int)i);
   if (want_jit && P.rb) {
-    pd->jit_error = jit_build(tp->info, P, c64, pd->jit, &pd->jit_ms, &pd->jit_compiled, &pd->jit_cached);
+    pd->jit_error = jit_build(tp->info, P, c64, fuse, pd->jit, &pd->jit_ms, &pd->jit_compiled, &pd->jit_cached);
     if (!pd->jit_error.empty()) pd->jit.clear();  // generic kernel for every pass
   }
+  if (fuse && !pd->jit.empty())  // executed flops of the fused NVRTC kernels
+    for (size_t i = 0; i < P.passes.size(); ++i)
+      if (P.passes[i].phase_count && pd->jit[i].kern) pd->pflops[i] = pass_flops_fused(tp->info, P, (int)i);
   *out = pd.get();
   tp->plans[key] = std::move(pd);
   return QSB_OK;
@@ -519,7 +523,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "engine") ctx->opt_engine = value;  // -1 auto, 0 resident, 1 streaming
   else if (k == "jit") ctx->opt_jit = value;        // NVRTC per-pass kernels (1) or generic kernel (0)
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
-  else if (k == "dedup") ctx->opt_dedup = value;    // branch-history deduplication of trajectories
+  else if (k == "dedup") ctx->opt_dedup = value;
+  else if (k == "fuse") ctx->opt_fuse = value;      // register-phase gate fusion in the NVRTC kernels    // branch-history deduplication of trajectories
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
     ctx->opt_reg_bits = value;
@@ -1571,9 +1576,40 @@ extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqu
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   int nk = 0;
   double ms = 0;
-  e = jit_compile_only(t, P, c64, &nk, &ms);
+  e = jit_compile_only(t, P, c64, true, &nk, &ms);
   out[0] = nk;
   out[1] = ms;
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  return QSB_OK;
+}
+
+extern "C" int32_t qsb_fusion_stats(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits,
+                                    int32_t nparams, int32_t precision, int32_t reg_bits, double* out) {
+  const int c64 = precision == QSB_C64 ? 1 : 0;
+  if (reg_bits < 3 || reg_bits > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
+  TapeInfo t;
+  std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  StreamPlan P;
+  e = build_stream_plan(t, 12, c64 ? 5 : 4, reg_bits, swizzle_bits(c64), P);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  const int fail0 = fuse_check_failures();
+  double st[6] = {0, 0, 0, 0, 0, 0};
+  for (size_t ph = 0; ph < P.phases.size(); ++ph) {
+    if (P.phases[ph].nt < 0) continue;
+    st[0] += 1;
+    for (const FuseItem& f : fuse_phase(t, P, (int)ph, true))
+      if (f.gate < 0) {
+        st[1] += 1;
+        st[2] += f.ngates;
+      }
+  }
+  for (size_t i = 0; i < P.passes.size(); ++i)
+    if (P.passes[i].phase_count) {
+      st[4] += pass_flops(t, P, (int)i);
+      st[5] += pass_flops_fused(t, P, (int)i);
+    }
+  st[3] = fuse_check_failures() - fail0;
+  for (int i = 0; i < 6; ++i) out[i] = st[i];
   return QSB_OK;
 }

@@ -185,8 +185,46 @@ std::string sparse_helper(uint32_t z) {
   return o.str();
 }
 
+// one fused block (qsb_plan.h fuse_phase): a dense 2x2 / 4x4 over register bits qa (matrix
+// bit 0) and qb (bit 1) with its entries at qsb_cf[cf ...]; exact-zero parts dropped
+void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr) {
+  const int d = f.qb < 0 ? 2 : 4;
+  const int A = 1 << f.qa, B = f.qb < 0 ? 0 : 1 << f.qb;
+  o << "  {  // fused block of " << f.ngates << " gates on register bits " << f.qa;
+  if (f.qb >= 0) o << ", " << f.qb;
+  o << "\n";
+  for (int j = 0; j < nr; ++j) {
+    if ((j & A) || (j & B)) continue;
+    const int idx[4] = {j, j | A, j | B, j | A | B};
+    o << "  { const A";
+    for (int c = 0; c < d; ++c) o << (c ? ", " : " ") << "x" << c << " = v" << idx[c];
+    o << ";\n";
+    for (int r = 0; r < d; ++r) {
+      auto chain = [&](bool im) {
+        std::string acc;
+        for (int c = d - 1; c >= 0; --c) {
+          const int e = 2 * (r * d + c);
+          // re: mr*x.x - mi*x.y ; im: mr*x.y + mi*x.x
+          const struct { int k; const char* x; bool neg; } terms[2] = {
+              {e + 1, im ? ".x" : ".y", !im}, {e, im ? ".y" : ".x", false}};
+          for (const auto& tm : terms) {
+            if (f.m[tm.k] == 0.0) continue;
+            const std::string coef = std::string(tm.neg ? "-" : "") + "qsb_cf[" + std::to_string(cf + tm.k) + "]";
+            const std::string x = "x" + std::to_string(c) + tm.x;
+            acc = acc.empty() ? coef + " * " + x : "fma(" + coef + ", " + x + ", " + acc + ")";
+          }
+        }
+        return acc.empty() ? std::string("(R)0") : acc;
+      };
+      o << "    v" << idx[r] << " = qsb::mk<R>(" << chain(false) << ", " << chain(true) << ");\n";
+    }
+    o << "  }\n";
+  }
+  o << "  }\n";
+}
+
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
-                const PhaseDesc& ph, int sb) {
+                const PhaseDesc& ph, int sb, const std::vector<FuseItem>& items, int cf0) {
   const int nr = 1 << P.rb;  // amplitudes per thread
   o << "__device__ __noinline__ void ph" << ph_index
     << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
@@ -195,8 +233,14 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
   for (int i = 0; i < ph.nt; ++i) o << " | ((((uint32_t)tid >> " << i << ") & 1u) << " << (int)ph.tpos[i] << ")";
   o << ";\n  const uint32_t sb = base ^ swz[base >> " << sb << "];\n";
   for (int j = 0; j < nr; ++j) o << "  A v" << j << " = tile[sb ^ " << ph.soff[j] << "u];\n";
-  for (int gl = 0; gl < ph.gate_count; ++gl) {
-    const int gidx = ph.gate_begin + gl;
+  int cf = cf0;
+  for (const FuseItem& item : items) {
+    if (item.gate < 0) {
+      emit_block(o, item, cf, nr);
+      cf += item.qb < 0 ? 8 : 32;
+      continue;
+    }
+    const int gidx = item.gate;
     const PhaseGate& q = P.phase_gates[gidx];
     const int gi = gidx - pd.pgate_begin;
     const MatSrc& ms = t.mats[q.mat];
@@ -294,9 +338,18 @@ bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass) {
   return false;
 }
 
-std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
+std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64, bool fuse) {
   const PassDesc& pd = P.passes[pass];
   const int sb = c64 ? 4 : 3;
+  std::vector<std::vector<FuseItem>> items(pd.phase_count);
+  std::vector<int> cf0(pd.phase_count, 0);
+  std::vector<double> cfv;  // fused-block matrices of the pass
+  for (int i = 0; i < pd.phase_count; ++i) {
+    items[i] = fuse_phase(t, P, pd.phase_begin + i, fuse);
+    cf0[i] = (int)cfv.size();
+    for (const FuseItem& f : items[i])
+      if (f.gate < 0) cfv.insert(cfv.end(), f.m, f.m + (f.qb < 0 ? 8 : 32));
+  }
   std::ostringstream o;
   for (const char* part : kJitPreludeParts) o << part;
   o << "\ntypedef " << (c64 ? "float" : "double") << " R;\ntypedef " << (c64 ? "float2" : "double2") << " A;\n";
@@ -328,9 +381,19 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
     if (!pd.pgate_count) o << "0";
     o << "};\n";
   }
+  if (!cfv.empty()) {
+    o << "__constant__ R qsb_cf[" << cfv.size() << "] = {";
+    for (size_t i = 0; i < cfv.size(); ++i) {
+      char buf[64];
+      if (c64) snprintf(buf, sizeof(buf), "%af", (double)(float)cfv[i]);
+      else snprintf(buf, sizeof(buf), "%a", cfv[i]);
+      o << (i ? ", " : "") << buf;
+    }
+    o << "};\n";
+  }
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
-    if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb);
+    if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb, items[i], cf0[i]);
   }
   const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
   o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pd.k - P.rb)) << ", " << (mb && *mb ? atoi(mb) : 2)
@@ -349,7 +412,7 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   return o.str();
 }
 
-std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vector<JitKernel>& out,
+std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, std::vector<JitKernel>& out,
                       double* compile_ms, int* compiled, int* cached) {
   auto t0 = std::chrono::steady_clock::now();
   out.assign(P.passes.size(), JitKernel());
@@ -369,7 +432,7 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vect
     if (P.passes[i].phase_count == 0) continue;
     Job j;
     j.pass = i;
-    j.src = jit_source(t, P, i, c64);
+    j.src = jit_source(t, P, i, c64, fuse);
     std::string key = j.src;
     for (const char* opt : kOpts) key += opt;
     char name[64];
@@ -441,14 +504,14 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vect
   return "";
 }
 
-std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, int* kernels, double* ms) {
+std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, int* kernels, double* ms) {
   auto t0 = std::chrono::steady_clock::now();
   *kernels = 0;
   for (int i = 0; i < (int)P.passes.size(); ++i) {
     if (P.passes[i].phase_count == 0) continue;
     std::vector<char> cubin;
     std::string log;
-    const std::string src = jit_source(t, P, i, c64);
+    const std::string src = jit_source(t, P, i, c64, fuse);
     if (const char* d = getenv("QSB_JIT_DUMP")) {  // debug: keep the generated sources
       std::ofstream f(std::string(d) + "/pass" + std::to_string(i) + ".cu");
       f << src;

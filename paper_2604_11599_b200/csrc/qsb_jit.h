@@ -27,14 +27,14 @@ bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass);
 // Generates, compiles (parallel, cached by source hash in $QSB_JIT_CACHE or
 // /tmp/qsb_jit_cache) and loads one kernel per register-blocked pass of `P`.
 // out[i] stays empty for passes without phases.  Returns "" or an error.
-std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, std::vector<JitKernel>& out,
+std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, std::vector<JitKernel>& out,
                       double* compile_ms, int* compiled, int* cached);
 
 // compile every pass kernel without loading it (host-only self test)
-std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, int* kernels, double* ms);
+std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, int* kernels, double* ms);
 
 // the generated CUDA source of pass `pass` (debug / tests)
-std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64);
+std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64, bool fuse);
 
 cudaError_t jit_launch(const JitKernel& jk, const StreamArgs& a, const PassDesc& pd, cudaStream_t s);
 void jit_release(std::vector<JitKernel>& ks);

@@ -18,8 +18,11 @@
 #include "qsb_plan.h"
 
 #include <algorithm>
+#include <atomic>
+#include <complex>
 #include <map>
 #include <cmath>
+#include <functional>
 #include <sstream>
 
 namespace qsb {
@@ -679,6 +682,296 @@ double pass_flops(const TapeInfo& t, const StreamPlan& P, int pass) {
     const PhaseGate& q = P.phase_gates[g];
     const int ctrl = popc(q.cmR) + popc(q.cmT) + popc(q.gcm);
     f += phase_gate_flops(q, t.mats[q.mat]) * std::ldexp(1.0, t.n - 1 - ctrl);
+  }
+  return f;
+}
+
+
+// ---------------------------------------------------------------------------
+// register-phase gate fusion (see qsb_plan.h)
+// ---------------------------------------------------------------------------
+namespace {
+
+using cd = std::complex<double>;
+std::atomic<int> g_fuse_fail{0};
+
+bool fusable(const TapeInfo& t, const PhaseGate& q) {
+  if (q.kind != PK_DENSE && q.kind != PK_XPERM && q.kind != PK_ANTI && q.kind != PK_DIAG_R) return false;
+  return q.guard < 0 && q.gcm == 0 && q.cmT == 0 && t.mats[q.mat].has_matrix && popc(q.cmR) <= 1 &&
+         !(q.cmR >> q.jt & 1);
+}
+
+// the 2x2 a register-phase gate applies to its (bit jt = 0, 1) pairs, as the kernels compute it
+void gate2x2(const TapeInfo& t, const PhaseGate& q, cd u[4]) {
+  const double* m = t.mats[q.mat].mat;
+  switch (q.kind) {
+    case PK_XPERM: u[0] = 0.0; u[1] = 1.0; u[2] = 1.0; u[3] = 0.0; break;
+    case PK_ANTI: u[0] = 0.0; u[1] = cd(m[2], m[3]); u[2] = cd(m[4], m[5]); u[3] = 0.0; break;
+    case PK_DIAG_R:
+      u[0] = q.diag_one0 ? cd(1.0, 0.0) : cd(m[0], m[1]);
+      u[1] = 0.0; u[2] = 0.0; u[3] = cd(m[6], m[7]);
+      break;
+    default:
+      for (int i = 0; i < 4; ++i) u[i] = cd(m[2 * i], m[2 * i + 1]);
+  }
+}
+
+// register bits a phase gate reads or writes
+uint32_t gate_bits(const PhaseGate& q) {
+  switch (q.kind) {
+    case PK_DENSE: case PK_XPERM: case PK_ANTI: case PK_DIAG_R: return q.cmR | (1u << q.jt);
+    case PK_DIAG_T: case PK_DIAG_G: return q.cmR;
+    default: return ~0u;
+  }
+}
+
+// flops per pair of a gate applied on its own (the JIT kernels' zero-dropped chains)
+double gate_pair_flops(const TapeInfo& t, const PhaseGate& q) { return phase_gate_flops(q, t.mats[q.mat]); }
+
+double chain_flops(const cd* row, int nc) {  // one output amplitude: re and im chains
+  int terms = 0;
+  for (int c = 0; c < nc; ++c) terms += (row[c].real() != 0.0) + (row[c].imag() != 0.0);
+  return terms ? 2.0 * (2.0 * (terms - 1) + 1.0) : 0.0;
+}
+
+struct Block {
+  int qa = -1, qb = -1;       // register bits (qb = -1: single qubit)
+  std::vector<int> gates;     // phase-gate indices in application order
+};
+
+// product matrix of a block: index bit 0 <-> qa, bit 1 <-> qb
+void block_matrix(const TapeInfo& t, const StreamPlan& P, const Block& b, cd* M) {
+  const int d = b.qb < 0 ? 2 : 4;
+  for (int i = 0; i < d * d; ++i) M[i] = (i % (d + 1) == 0) ? 1.0 : 0.0;
+  for (int gi : b.gates) {
+    const PhaseGate& q = P.phase_gates[gi];
+    cd u[4];
+    gate2x2(t, q, u);
+    const int tb = q.jt == b.qa ? 0 : 1;  // matrix bit of the target
+    const int cb = q.cmR ? 1 - tb : -1;    // matrix bit of the control
+    const int cval = q.cmR ? (q.cvR ? 1 : 0) : 0;
+    cd G[16];
+    for (int i = 0; i < d * d; ++i) G[i] = 0.0;
+    for (int r = 0; r < d; ++r)
+      for (int c = 0; c < d; ++c) {
+        if ((r & ~(1 << tb)) != (c & ~(1 << tb))) continue;  // other bits unchanged
+        if (cb >= 0 && ((r >> cb) & 1) != cval) {
+          G[r * d + c] = r == c ? 1.0 : 0.0;
+          continue;
+        }
+        G[r * d + c] = u[((r >> tb) & 1) * 2 + ((c >> tb) & 1)];
+      }
+    cd N[16];
+    for (int r = 0; r < d; ++r)
+      for (int c = 0; c < d; ++c) {
+        cd s = 0.0;
+        for (int x = 0; x < d; ++x) s += G[r * d + x] * M[x * d + c];
+        N[r * d + c] = s;
+      }
+    for (int i = 0; i < d * d; ++i) M[i] = N[i];
+  }
+}
+
+// host emulation of items on a register vector (check of the fusion)
+void emulate(const TapeInfo& t, const StreamPlan& P, const std::vector<FuseItem>& items, int nr, cd* v) {
+  for (const FuseItem& it : items) {
+    if (it.gate >= 0) {
+      const PhaseGate& q = P.phase_gates[it.gate];
+      if (q.kind == PK_DIAG_T || q.kind == PK_DIAG_G) {
+        const cd f(t.mats[q.mat].mat[0] + 0.25, t.mats[q.mat].mat[1] - 0.5);
+        for (int j = 0; j < nr; ++j)
+          if (((uint32_t)j & q.cmR) == q.cvR) v[j] *= f;
+        continue;
+      }
+      cd u[4];
+      gate2x2(t, q, u);
+      const int b = 1 << q.jt;
+      for (int j = 0; j < nr; ++j) {
+        if ((j & b) || ((uint32_t)j & q.cmR) != q.cvR) continue;
+        const cd a0 = v[j], a1 = v[j | b];
+        v[j] = u[0] * a0 + u[1] * a1;
+        v[j | b] = u[2] * a0 + u[3] * a1;
+      }
+      continue;
+    }
+    const int A = 1 << it.qa, B = it.qb < 0 ? 0 : 1 << it.qb, d = it.qb < 0 ? 2 : 4;
+    for (int j = 0; j < nr; ++j) {
+      if ((j & A) || (j & B)) continue;
+      const int idx[4] = {j, j | A, j | B, j | A | B};
+      cd x[4], y[4];
+      for (int c = 0; c < d; ++c) x[c] = v[idx[c]];
+      for (int r = 0; r < d; ++r) {
+        y[r] = 0.0;
+        for (int c = 0; c < d; ++c) y[r] += cd(it.m[2 * (r * d + c)], it.m[2 * (r * d + c) + 1]) * x[c];
+      }
+      for (int r = 0; r < d; ++r) v[idx[r]] = y[r];
+    }
+  }
+}
+
+}  // namespace
+
+double fuse_block_flops(const FuseItem& f) {
+  const int d = f.qb < 0 ? 2 : 4;
+  double s = 0;
+  for (int r = 0; r < d; ++r) {
+    cd row[4];
+    for (int c = 0; c < d; ++c) row[c] = cd(f.m[2 * (r * d + c)], f.m[2 * (r * d + c) + 1]);
+    s += chain_flops(row, d);
+  }
+  return s;
+}
+
+int fuse_check_failures() { return g_fuse_fail.load(); }
+
+std::vector<FuseItem> fuse_phase(const TapeInfo& t, const StreamPlan& P, int phase, bool enable) {
+  const PhaseDesc& ph = P.phases[phase];
+  std::vector<FuseItem> plain;
+  for (int g = ph.gate_begin; g < ph.gate_begin + ph.gate_count; ++g) {
+    FuseItem f;
+    f.gate = g;
+    plain.push_back(f);
+  }
+  if (!enable || ph.nt < 0 || ph.gate_count < 2) return plain;
+  const int rb = P.rb;
+  std::vector<FuseItem> out;
+  std::vector<Block> blocks;       // open blocks (by id)
+  std::vector<int> open(rb, -1);   // register bit -> open block id
+  std::vector<bool> live;
+  auto new_block = [&](int qa, int qb) {
+    blocks.push_back(Block{qa, qb, {}});
+    live.push_back(true);
+    const int id = (int)blocks.size() - 1;
+    open[qa] = id;
+    if (qb >= 0) open[qb] = id;
+    return id;
+  };
+  auto emit_gate = [&](int g) {
+    FuseItem f;
+    f.gate = g;
+    out.push_back(f);
+  };
+  // close block id: fused if cheaper; otherwise its gates one by one, except that the
+  // single-qubit gates after its last two-qubit gate stay open (keep_tail) so that a
+  // later block can absorb them
+  std::function<void(int, bool)> close = [&](int id, bool keep_tail) {
+    if (!live[id]) return;
+    live[id] = false;
+    Block b = blocks[id];
+    if (open[b.qa] == id) open[b.qa] = -1;
+    if (b.qb >= 0 && open[b.qb] == id) open[b.qb] = -1;
+    double sep = 0;
+    for (int gi : b.gates) {
+      const PhaseGate& q = P.phase_gates[gi];
+      const double pairs = b.qb < 0 ? 1.0 : (q.cmR ? 1.0 : 2.0);  // pairs per group of the block
+      sep += gate_pair_flops(t, q) * pairs;
+    }
+    if (b.gates.size() >= 2) {
+      FuseItem f;
+      f.qa = b.qa;
+      f.qb = b.qb;
+      f.ngates = (int)b.gates.size();
+      cd M[16];
+      block_matrix(t, P, b, M);
+      const int d = b.qb < 0 ? 2 : 4;
+      for (int i = 0; i < d * d; ++i) {
+        f.m[2 * i] = M[i].real();
+        f.m[2 * i + 1] = M[i].imag();
+      }
+      if (fuse_block_flops(f) < sep) {
+        out.push_back(f);
+        return;
+      }
+    }
+    int last2 = -1;
+    if (keep_tail && b.qb >= 0)
+      for (int i = 0; i < (int)b.gates.size(); ++i)
+        if (P.phase_gates[b.gates[i]].cmR) last2 = i;
+    if (!keep_tail || b.qb < 0 || last2 < 0) {
+      for (int gi : b.gates) emit_gate(gi);
+      return;
+    }
+    for (int i = 0; i <= last2; ++i) emit_gate(b.gates[i]);
+    for (int i = last2 + 1; i < (int)b.gates.size(); ++i) {
+      const int gi = b.gates[i];
+      const int q = P.phase_gates[gi].jt;
+      if (open[q] < 0) new_block(q, -1);
+      blocks[open[q]].gates.push_back(gi);
+    }
+  };
+  for (int g = ph.gate_begin; g < ph.gate_begin + ph.gate_count; ++g) {
+    const PhaseGate& q = P.phase_gates[g];
+    if (!fusable(t, q)) {
+      const uint32_t bits = gate_bits(q);
+      for (int r = 0; r < rb; ++r)
+        if ((bits >> r & 1) && open[r] >= 0) close(open[r], false);
+      emit_gate(g);
+      continue;
+    }
+    if (!q.cmR) {
+      if (open[q.jt] < 0) new_block(q.jt, -1);
+      blocks[open[q.jt]].gates.push_back(g);
+      continue;
+    }
+    const int a = q.jt, c = __builtin_ctz(q.cmR);
+    if (open[a] >= 0 && open[a] == open[c]) {
+      blocks[open[a]].gates.push_back(g);
+      continue;
+    }
+    for (int x : {a, c})
+      if (open[x] >= 0 && blocks[open[x]].qb >= 0) close(open[x], true);
+    std::vector<int> pre;
+    for (int x : {a, c})
+      if (open[x] >= 0) {
+        const int id = open[x];
+        pre.insert(pre.end(), blocks[id].gates.begin(), blocks[id].gates.end());
+        live[id] = false;
+        open[x] = -1;
+      }
+    const int id = new_block(std::min(a, c), std::max(a, c));
+    blocks[id].gates = pre;
+    blocks[id].gates.push_back(g);
+  }
+  for (int id = 0; id < (int)blocks.size(); ++id) close(id, false);
+  // host check: the items reproduce the gates on random register vectors
+  const int nr = 1 << rb;
+  uint64_t s = 0x9E3779B97F4A7C15ull ^ (uint64_t)phase;
+  auto rnd = [&]() {
+    s = s * 6364136223846793005ull + 1442695040888963407ull;
+    return (double)(s >> 11) * 0x1.0p-53 - 0.5;
+  };
+  for (int trial = 0; trial < 2; ++trial) {
+    std::vector<cd> v(nr), w(nr);
+    for (int j = 0; j < nr; ++j) v[j] = w[j] = cd(rnd(), rnd());
+    emulate(t, P, plain, nr, v.data());
+    emulate(t, P, out, nr, w.data());
+    double err = 0, mag = 0;
+    for (int j = 0; j < nr; ++j) {
+      err = std::max(err, std::abs(v[j] - w[j]));
+      mag = std::max(mag, std::abs(v[j]));
+    }
+    if (!(err <= 1e-12 * std::max(1.0, mag))) {
+      ++g_fuse_fail;
+      return plain;
+    }
+  }
+  return out;
+}
+
+double pass_flops_fused(const TapeInfo& t, const StreamPlan& P, int pass) {
+  const PassDesc& pd = P.passes[pass];
+  double f = 0;
+  for (int i = 0; i < pd.phase_count; ++i) {
+    const int phase = pd.phase_begin + i;
+    for (const FuseItem& it : fuse_phase(t, P, phase, true)) {
+      if (it.gate >= 0) {
+        const PhaseGate& q = P.phase_gates[it.gate];
+        const int ctrl = popc(q.cmR) + popc(q.cmT) + popc(q.gcm);
+        f += phase_gate_flops(q, t.mats[q.mat]) * std::ldexp(1.0, t.n - 1 - ctrl);
+      } else {
+        f += fuse_block_flops(it) * std::ldexp(1.0, t.n - (it.qb < 0 ? 1 : 2));
+      }
+    }
   }
   return f;
 }

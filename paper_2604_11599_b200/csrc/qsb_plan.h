@@ -66,3 +66,31 @@ double pass_flops(const TapeInfo& t, const StreamPlan& P, int pass);
 std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz_bits, StreamPlan& out);
 
 }  // namespace qsb
+
+namespace qsb {
+
+// ---------------------------------------------------------------------------
+// Gate fusion inside a register phase (NVRTC kernels).  Literal, unguarded gates on
+// register bits are collected into 1- and 2-qubit blocks (commutation on disjoint
+// qubits); a block whose product matrix costs fewer FP operations per amplitude than
+// its gates applied one by one is emitted as one dense 2x2 / 4x4 (e.g. the four `u`
+// gates around a cx of a brick layer: 4 x 24 x 2 flops per 4 amplitudes -> 120).
+// ---------------------------------------------------------------------------
+struct FuseItem {
+  int gate = -1;         // >= 0: emit phase gate P.phase_gates[gate] unchanged
+  int qa = -1, qb = -1;  // fused block: register bits of matrix index bit 0 / bit 1 (qb = -1: 2x2)
+  int ngates = 0;        // gates folded into the block
+  double m[32];          // row-major complex entries (re, im); a 2x2 uses m[0..7]
+};
+// items of phase `phase` (index into P.phases) in emission order; `enable` = false
+// returns the gates one by one.  Every fused phase is checked on the host against its
+// gates on random register vectors; a mismatch falls back to the unfused list.
+std::vector<FuseItem> fuse_phase(const TapeInfo& t, const StreamPlan& P, int phase, bool enable);
+// flops of one fused block per group of 2 (2x2) or 4 (4x4) amplitudes, zero components dropped
+double fuse_block_flops(const FuseItem& f);
+// pass_flops with the fused blocks of the NVRTC kernels
+double pass_flops_fused(const TapeInfo& t, const StreamPlan& P, int pass);
+// number of fused phases whose host check failed (diagnostics; should stay 0)
+int fuse_check_failures();
+
+}  // namespace qsb

@@ -237,20 +237,53 @@ def test_jit_kernels_bit_identical_to_generic(prec):
     k = workloads.random_static(15, 400, seed=77, nparams=4, max_controls=2)
     vals = [0.3, -1.1, 2.2, 0.7]
     b = ir.bind(k, vals)
-    with option("jit", 0, 1):
-        generic = sim.statevector(b, precision=prec).amps
-    jit = sim.statevector(b, precision=prec).amps
-    assert sim.last_stats()["jit_passes"] > 0
-    np.testing.assert_array_equal(jit, generic)
-    assert_state(jit, P.final_state(b).amps, TOL[prec])
+    with option("fuse", 0, 1):  # gate fusion changes the arithmetic (tested below)
+        with option("jit", 0, 1):
+            generic = sim.statevector(b, precision=prec).amps
+        jit = sim.statevector(b, precision=prec).amps
+        assert sim.last_stats()["jit_passes"] > 0
+        np.testing.assert_array_equal(jit, generic)
+        assert_state(jit, P.final_state(b).amps, TOL[prec])
+        _, kd = workloads.dyn_circuit(n=16, layers=10, every=5, nmeas=3, seed=21)
+        bd = ir.bind(kd, [])
+        with option("jit", 0, 1):
+            w0, tape = sim.sample_words(bd, 64, 9, precision=prec)
+        w1, _ = sim.sample_words(bd, 64, 9, precision=prec)
+        np.testing.assert_array_equal(w0, w1)
+        if prec == "c128":
+            assert tape.keys(w1) == P.trajectory_keys(bd, 9, 0, 64)
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_fused_blocks_match_oracle(prec):
+    """Register-phase gate fusion (dense 2x2 / 4x4 products of literal gates, NVRTC
+    kernels): the fused kernels run fewer FP operations than the unfused ones and
+    agree with the oracle within the precision's tolerance; c128 trajectories of a
+    u-brick dynamic circuit stay bit-exact."""
     _, kd = workloads.dyn_circuit(n=16, layers=10, every=5, nmeas=3, seed=21)
     bd = ir.bind(kd, [])
-    with option("jit", 0, 1):
-        w0, tape = sim.sample_words(bd, 64, 9, precision=prec)
-    w1, _ = sim.sample_words(bd, 64, 9, precision=prec)
-    np.testing.assert_array_equal(w0, w1)
+    # the gates before the first measurement round: a static u-brick
+    first = []
+    for op in kd.body:
+        if not isinstance(op, ir.Gate):
+            break
+        first.append(op)
+    bs = ir.bind(ir.Kernel(kd.qubit_count, kd.qubit_layout, [], [], first), [])
+    ref = P.final_state(bs).amps
+    stats = {}
+    for fuse in (0, 1):
+        with option("fuse", fuse, 1):
+            st = sim.statevector(bs, precision=prec)
+            stats[fuse] = sim.last_stats()
+            assert stats[fuse]["jit_passes"] > 0
+            assert_state(st.amps, ref, TOL[prec])
+    assert stats[1]["pass_flops"] < 0.9 * stats[0]["pass_flops"], (stats[0]["pass_flops"], stats[1]["pass_flops"])
+    words, tape = sim.sample_words(bd, 64, 9, precision=prec)
     if prec == "c128":
-        assert tape.keys(w1) == P.trajectory_keys(bd, 9, 0, 64)
+        assert tape.keys(words) == P.trajectory_keys(bd, 9, 0, 64)
+    k = workloads.random_static(15, 400, seed=77, nparams=4, max_controls=2)
+    b = ir.bind(k, [0.3, -1.1, 2.2, 0.7])
+    assert_state(sim.statevector(b, precision=prec).amps, P.final_state(b).amps, TOL[prec])
 
 
 @pytest.mark.parametrize("prec", ["c128", "c64"])
