@@ -222,7 +222,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   PassItem cur;
   cur.alive = false;
   if (w < W) cur = pass_item(a, pd, w, ntl, itb);
-  if (NB == 2 && w < W) prefetch(cur, bufs);
+  if (w < W) prefetch(cur, bufs);
   cp_async_commit();
   int b = 0;
   for (; w < W; w += gridDim.x) {
@@ -235,8 +235,8 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
       cp_async_commit();
       cp_async_wait1();
     } else {
-      prefetch(cur, bufs);
-      cp_async_commit();
+      // single buffer: this item's gather was issued at the end of the previous item,
+      // concurrently with that item's scatter
       cp_async_wait0();
     }
     __syncthreads();
@@ -363,11 +363,29 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
       }
       A* st = reinterpret_cast<A*>(a.state) + (it.slot << a.n);
       const uint64_t pb = it.base_phys | Pt;
+      if (NB == 2) {
 #pragma unroll 4
-      for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = tile[St ^ ujt[j]];
+        for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = tile[St ^ ujt[j]];
+      } else {
+        // single buffer: take the tile into registers, release the buffer, start the
+        // next item's gather, then store -- the scatter and the next gather overlap
+        A v[1 << RB];
+#pragma unroll
+        for (int j = 0; j < (1 << RB); ++j) v[j] = tile[St ^ ujt[j]];
+        __syncthreads();
+        if (wn < W) prefetch(cur, bufs);
+        cp_async_commit();
+#pragma unroll
+        for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = v[j];
+        continue;
+      }
     }
     __syncthreads();
     if (NB == 2) b ^= 1;
+    else {
+      if (wn < W) prefetch(cur, bufs);  // dead item: nothing to store
+      cp_async_commit();
+    }
   }
   cp_async_wait0();
 }

@@ -18,6 +18,8 @@
 #include "qsb_plan.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <complex>
 #include <map>
@@ -933,6 +935,16 @@ std::vector<FuseItem> fuse_phase(const TapeInfo& t, const StreamPlan& P, int pha
     blocks[id].gates.push_back(g);
   }
   for (int id = 0; id < (int)blocks.size(); ++id) close(id, false);
+  if (getenv("QSB_FUSE_DEBUG")) {
+    fprintf(stderr, "phase %d:", phase);
+    for (const FuseItem& f : out) {
+      if (f.gate >= 0) {
+        const PhaseGate& q = P.phase_gates[f.gate];
+        fprintf(stderr, " g%d(k%d t%d c%x)", f.gate - ph.gate_begin, q.kind, q.jt, q.cmR);
+      } else fprintf(stderr, " [B%d,%d:%d]", f.qa, f.qb, f.ngates);
+    }
+    fprintf(stderr, "\n");
+  }
   // host check: the items reproduce the gates on random register vectors
   const int nr = 1 << rb;
   uint64_t s = 0x9E3779B97F4A7C15ull ^ (uint64_t)phase;
