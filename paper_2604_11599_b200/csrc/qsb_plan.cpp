@@ -243,6 +243,7 @@ struct Planner {
   const TapeInfo& t;
   int k, lowq, rb;
   int swz_bits_ = 3;
+  bool pair_aware_ = getenv("QSB_PAIR_AWARE") ? atoi(getenv("QSB_PAIR_AWARE")) != 0 : true;
   StreamPlan& P;
   std::vector<RegionBuild> regions;
 
@@ -282,7 +283,7 @@ struct Planner {
       }
       uint32_t R = 0, blocked = 0;
       std::vector<int> take, rest;
-      for (int gi : rem) {
+      for (const int& gi : rem) {
         const PassGate& g = P.gates[gi];
         uint32_t touched = g.lcm;
         if (g.gclass != GC_DIAG_GLOBAL) touched |= 1u << g.lt;
@@ -297,7 +298,19 @@ struct Planner {
         need &= ~R;
         // tile controls of a register-target gate: in the registers the controlled pairs
         // are chosen at compile time; on a thread position every pair costs selects
-        const uint32_t want = need ? (need | (g.lcm & ~R)) : 0;
+        uint32_t want = need ? (need | (g.lcm & ~R)) : 0;
+        // a single-qubit gate brings the partner of its next two-qubit gate along, so that
+        // the pair's gates can fuse into one 4x4 block (fuse_phase)
+        if (pair_aware_ && need && !g.lcm) {
+          for (size_t x = &gi - rem.data() + 1; x < rem.size(); ++x) {
+            const PassGate& h = P.gates[rem[x]];
+            const uint32_t ht = h.gclass == GC_DIAG_GLOBAL ? 0u : (1u << h.lt);
+            if (!((ht | h.lcm) >> g.lt & 1)) continue;
+            if (h.gclass != GC_DIAG_GLOBAL && h.gclass != GC_SWAP && popc(h.lcm) == 1)
+              want |= (ht | h.lcm) & ~R;
+            break;
+          }
+        }
         if (want && popc(R | want) <= rb) {
           R |= want;
           take.push_back(gi);
