@@ -338,6 +338,17 @@ bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass) {
   return false;
 }
 
+// buffering mode of a pass kernel (qsb_pass_common.cuh).  MODE 1 (two thread groups over
+// a three-tile ring, complex128) is opt-in ($QSB_PASS_MODE=1): measured on B200 it is
+// 6-20 % slower than MODE 0 (the per-item context loads and the mbarrier waits sit on
+// each group's critical path; ncu: long_scoreboard 18-27 % vs 6-12 %).
+int jit_pass_mode(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
+  const char* e = getenv("QSB_PASS_MODE");
+  if (c64 || !(e && *e && atoi(e) == 1)) return 0;
+  const size_t sm = pass_reg_smem(c64, P.passes[pass], P.rb, t.n, pass_needs_stage(t, P, pass), 1);
+  return sm <= 227 * 1024 ? 1 : 0;
+}
+
 std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64, bool fuse) {
   const PassDesc& pd = P.passes[pass];
   const int sb = c64 ? 4 : 3;
@@ -395,18 +406,20 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb, items[i], cf0[i]);
   }
-  const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
-  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pd.k - P.rb)) << ", " << (mb && *mb ? atoi(mb) : 2)
-    << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
-  o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
   const bool stage = pass_needs_stage(t, P, pass);
-  o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false")
+  const int mode = jit_pass_mode(t, P, pass, c64);
+  const int threads = pass_groups(mode) << (pd.k - P.rb);
+  const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
+  o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
+    << (mode == 1 ? 1 : (mb && *mb ? atoi(mb) : 2)) << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
+  o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+  o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false") << ", " << mode
     << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) o << "    ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";
     else o << "    qsb::pass_swap<R, " << sb << ">(cx, cx.sg[" << (ph.gate_begin - pd.pgate_begin) << "]);\n";
-    o << "    __syncthreads();\n";
+    o << "    cx.sync();\n";
   }
   o << "  });\n}\n";
   return o.str();
@@ -485,8 +498,9 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
     JitKernel& jk = out[j.pass];
     jk.lib = (void*)lib;
     jk.kern = (void*)k;
-    jk.smem = pass_reg_smem(c64, P.passes[j.pass], P.rb, t.n, pass_needs_stage(t, P, j.pass));
-    jk.threads = 1 << (P.passes[j.pass].k - P.rb);
+    const int mode = jit_pass_mode(t, P, j.pass, c64);
+    jk.smem = pass_reg_smem(c64, P.passes[j.pass], P.rb, t.n, pass_needs_stage(t, P, j.pass), mode);
+    jk.threads = pass_groups(mode) << (P.passes[j.pass].k - P.rb);
     e = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
     if (e != cudaSuccess) {
       jit_release(out);

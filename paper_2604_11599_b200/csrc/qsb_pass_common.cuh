@@ -35,12 +35,20 @@ template <int SB> __device__ __forceinline__ uint32_t swz_slot(const uint32_t* s
   return l ^ swz[l >> SB];
 }
 
+// named barrier of a thread group (0: __syncthreads of the whole CTA)
+__device__ __forceinline__ void group_sync(int bar, int nthreads) {
+  if (bar == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nthreads) : "memory");
+}
+
 // the shared-memory context handed to the phase code
 template <typename R> struct PassCtx {
   typename Amp<R>::T* tile;
   SGate<R>* sg;
   uint32_t* swz;
   int tid, T, TL;
+  int bar;  // barrier of the thread group working on `tile`
+  __device__ __forceinline__ void sync() const { group_sync(bar, T); }
 };
 
 // per work-item (slot, tile) view of the trajectory control block
@@ -124,21 +132,49 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// Buffering mode: complex64 tiles (32 KiB) double-buffer in shared memory (two CTAs per
-// SM still fit); complex128 tiles (64 KiB) keep one buffer so that two CTAs share an SM,
-// and the two CTAs' gather / compute / scatter phases overlap each other.  (Measured:
-// an L2 prefetch of the next item -- bulk or per line -- and one double-buffered CTA
-// per SM were both slower.)
-__host__ __device__ inline int pass_buffers(int c64) { return c64 ? 2 : 1; }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {  // release: plain shared stores before it are visible
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* b) {  // fires when this thread's cp.async land
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nQSB_MBW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra QSB_MBW;\n}\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// Buffering modes of the persistent driver.
+//   MODE 0: each CTA (2 per SM) walks its items alone: complex64 tiles (32 KiB)
+//           double-buffer; complex128 tiles (64 KiB) keep one buffer, whose scatter
+//           overlaps the next gather, and the two CTAs of an SM overlap each other.
+//   MODE 1 (complex128, NVRTC kernels): one CTA per SM with two thread groups and a
+//           ring of three tile buffers.  Local item i runs on group i % 2 in buffer
+//           i % 3; when a group has taken item i into registers it issues the gather of
+//           item i + 3 into the same buffer (consumed by the other group), so every
+//           gather is in flight while both groups compute.  Completion is signalled
+//           through mbarriers (cp.async.mbarrier.arrive) indexed i % 6, which keeps
+//           the parity of a wait unambiguous (item i - 6 ran on the same group).
+__host__ __device__ inline int pass_buffers(int c64, int mode) { return mode == 1 ? 3 : (c64 ? 2 : 1); }
+__host__ __device__ inline int pass_groups(int mode) { return mode == 1 ? 2 : 1; }
 
 // dynamic shared memory of a register-blocked pass
-__host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int rb, int n, bool stage) {
+__host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int rb, int n, bool stage, int mode = 0) {
   const int sb = c64 ? 4 : 3;
   const size_t amp = c64 ? 8 : 16;
   const size_t sgate = c64 ? 64 : 96;
-  return pass_buffers(c64) * (amp << pd.k) + (stage ? sgate * pd.pgate_count : 0) +
+  const int G = pass_groups(mode);
+  return pass_buffers(c64, mode) * (amp << pd.k) + G * (stage ? sgate * pd.pgate_count : 0) +
          (sizeof(uint64_t) << (pd.k - pd.lowq)) + (sizeof(uint32_t) << (pd.k - sb)) +
-         sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) + item_tables_bytes(n) + 16;
+         G * sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) + item_tables_bytes(n) + 16 +
+         (mode == 1 ? 6 * (sizeof(uint64_t) + sizeof(PassItem)) + 16 : 0);
 }
 
 
@@ -147,34 +183,46 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
 // false when none of their phases reads the staged gates (literal matrices from the
 // constant bank, no per-item decisions), which removes a global-load round trip and a
 // barrier from every item.
-template <typename R, int RB, bool STAGE = true, typename PhaseRunner>
+template <typename R, int RB, bool STAGE = true, int MODE = 0, typename PhaseRunner>
 __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassDesc& pd, unsigned char* smem_raw,
                                                 PhaseRunner run) {
   using A = typename Amp<R>::T;
   constexpr int SB = sizeof(R) == 8 ? 3 : 4;
-  const int k = pd.k, TL = 1 << k, T = TL >> RB, tid = threadIdx.x;
-  constexpr int NB = sizeof(R) == 4 ? 2 : 1;  // pass_buffers()
+  constexpr int G = MODE == 1 ? 2 : 1;  // thread groups
+  constexpr int NB = MODE == 1 ? 3 : (sizeof(R) == 4 ? 2 : 1);  // pass_buffers()
+  const int k = pd.k, TL = 1 << k, T = TL >> RB;
+  const int grp = MODE == 1 ? (int)(threadIdx.x >= (unsigned)T) : 0;
+  const int tid = (int)threadIdx.x - grp * T;  // thread index inside the group
+  const int ctid = threadIdx.x, CT = G * T;    // whole CTA (table set-up)
+  const int bar = MODE == 1 ? 1 + grp : 0;
   A* bufs = reinterpret_cast<A*>(smem_raw);
-  SGate<R>* sg = reinterpret_cast<SGate<R>*>(bufs + NB * TL);
-  uint64_t* hi_off = reinterpret_cast<uint64_t*>(sg + (STAGE ? pd.pgate_count : 0));
+  SGate<R>* sg0 = reinterpret_cast<SGate<R>*>(bufs + NB * TL);
+  SGate<R>* sg = sg0 + (STAGE ? grp * pd.pgate_count : 0);
+  uint64_t* hi_off = reinterpret_cast<uint64_t*>(sg0 + (STAGE ? G * pd.pgate_count : 0));
   uint32_t* swz = reinterpret_cast<uint32_t*>(hi_off + (TL >> pd.lowq));
-  double* red = reinterpret_cast<double*>(swz + (TL >> SB));
-  uint32_t* ujt = reinterpret_cast<uint32_t*>(red + T);  // [2^RB] swizzled slot of j*T
+  double* red0 = reinterpret_cast<double*>(swz + (TL >> SB));
+  double* red = red0 + grp * T;
+  uint32_t* ujt = reinterpret_cast<uint32_t*>(red0 + G * T);  // [2^RB] swizzled slot of j*T
   ItemTables itb;
   itb.pdt = reinterpret_cast<uint64_t*>((reinterpret_cast<size_t>(ujt + (1 << RB)) + 15) & ~(size_t)15);
   itb.pxo = itb.pdt + item_chunks(a.n) * 16;
   itb.pxs = reinterpret_cast<uint32_t*>(itb.pxo + item_chunks(a.n) * 16);
-  build_item_tables(itb, pd, a.n, tid, T);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(((reinterpret_cast<size_t>(itb.pxs + item_chunks(a.n) * 16)) + 7) &
+                                               ~(size_t)7);
+  build_item_tables(itb, pd, a.n, ctid, CT);
   const uint64_t lowm = (1ull << pd.lowq) - 1;
   const uint64_t shi = pd.smask & ~lowm;
-  for (int h = tid; h < (TL >> pd.lowq); h += T) hi_off[h] = pdep64((uint64_t)h, shi);
+  for (int h = ctid; h < (TL >> pd.lowq); h += CT) hi_off[h] = pdep64((uint64_t)h, shi);
   const uint8_t* V = SB == 3 ? c_swz3 : c_swz4;
-  for (int h = tid; h < (TL >> SB); h += T) {
+  for (int h = ctid; h < (TL >> SB); h += CT) {
     uint32_t s = 0;
     for (int p = SB, hh = h; hh; ++p, hh >>= 1)
       if (hh & 1) s ^= V[p];
     swz[h] = s;
   }
+  PassItem* ctxs = reinterpret_cast<PassItem*>(mbar + 6);  // MODE 1: item contexts, by local item % 6
+  if (MODE == 1 && ctid < 6) mbar_init(&mbar[ctid], T + 1);
+  if (MODE == 1) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
   // Tile element l = tid + j*T (j < 2^RB; tid and j*T occupy disjoint bits, and
   // T is a multiple of 2^lowq and of 2^SB).  pdep and the swizzle are both linear
@@ -184,14 +232,13 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   // and with the Pauli-X frame flip fl of an item the slot of l ^ fl is
   //   (Ft ^ G) ^ ujt[j], Ft = swizzled slot of tid ^ (fl & (T-1)), G = that of fl & ~(T-1).
   // The loops below therefore cost a few integer ops per amplitude.
-  if (tid < (1 << RB)) ujt[tid] = swz_slot<SB>(swz, (uint32_t)(tid * T));
+  if (ctid < (1 << RB)) ujt[ctid] = swz_slot<SB>(swz, (uint32_t)(ctid * T));
   const uint64_t Pt = ((uint64_t)tid & lowm) | hi_off[tid >> pd.lowq];
   const uint32_t St = swz_slot<SB>(swz, (uint32_t)tid);
   const int hstep = T >> pd.lowq;
   __syncthreads();
   const int ntl = a.n - k;
   const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << ntl;
-  const uint64_t qmask = (a.n >= 64) ? ~0ull : ((1ull << a.n) - 1);
 
   // swizzled-slot base of this thread for an item with frame flip fl
   auto flip_base = [&](uint32_t fl) -> uint32_t {
@@ -217,6 +264,172 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     }
   };
 
+  // One item on `tile` (gathered): pending collapse, gate staging, the phases, the
+  // epilogue marginal; leaves the tile in the registers v.
+  auto process = [&](const PassItem& it, A* tile, A* v) {
+    if (it.pending) {  // collapse of the previous decide: projection + complex scale
+      const R sre = (R)it.sre, sim = (R)it.sim;
+      const uint64_t pb = it.base_phys | Pt;
+      const uint32_t fb = flip_base(it.fl);
+      for (int j = 0; j < (1 << RB); ++j) {
+        const uint64_t p = pb | hi_off[j * hstep];
+        A* d = tile + (fb ^ ujt[j]);
+        A x = *d;
+        if ((p & it.Kp) != it.Vp) x = mk<R>(0, 0);
+        else x = mk<R>(fma(sre, x.x, -sim * x.y), fma(sre, x.y, sim * x.x));
+        *d = x;
+      }
+    }
+    if (STAGE) {  // stage the gates: guards, out-of-tile controls, per-CTA diagonal factors
+      const uint32_t* gw = a.guards + it.slot * a.gwords;
+      const double* mats = a.mats + it.slot * a.mat_stride;
+      for (int i = tid; i < pd.pgate_count; i += T) {
+        const PhaseGate g = a.phase_gates[pd.pgate_begin + i];
+        SGate<R> s;
+        double m[8];
+        const double* src = mats + (int64_t)g.mat * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = src[j];
+        int kind = g.kind;
+        bool skip = (g.guard >= 0 && !((gw[g.guard >> 5] >> (g.guard & 31)) & 1u)) ||
+                    ((it.base_log & g.gcm) != g.gcv);
+        if (kind == PK_DIAG_G) kind = PK_DIAG_T;  // same code path, tp = -1
+        if (kind == PK_DENSE) {
+          if (m[1] == 0.0 && m[3] == 0.0 && m[5] == 0.0 && m[7] == 0.0) kind = PK_DENSE_REAL;
+          else if (m[1] == 0.0 && m[7] == 0.0 && m[2] == 0.0 && m[4] == 0.0) kind = PK_DENSE_RX;
+        } else if (g.kind == PK_DIAG_G) {
+          int bb = (int)((it.base_log >> g.tp) & 1);
+          if (!bb && g.diag_one0) skip = true;
+          if (bb) {
+            m[0] = m[6];
+            m[1] = m[7];
+          }
+        }
+        s.kind = skip ? PK_SKIP : kind;
+        s.jt = g.kind == PK_DIAG_T ? g.diag_one0 : g.jt;
+        s.jt2 = g.jt2;
+        s.tp = (g.kind == PK_DIAG_T || g.kind == PK_SWAP_R) ? g.tp : -1;
+        s.cmR = g.cmR;
+        s.cvR = g.cvR;
+        s.cmT = g.cmT;
+        s.cvT = g.cvT;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s.m[j] = (R)m[j];
+        sg[i] = s;
+      }
+    }
+    if (STAGE || it.pending) group_sync(bar, T);
+    PassCtx<R> cx{tile, sg, swz, tid, T, TL, bar};
+    run(cx);  // the phases (each ends with cx.sync())
+    if (pd.epi) {  // per-tile marginal of the next region's measured qubits (fixed order)
+      const int ml = pd.m_local;
+      const int nb = 1 << ml;
+      uint32_t mlm = 0;
+      for (int j = 0; j < ml; ++j) mlm |= 1u << pd.mloc[j];
+      const uint32_t free_mask = ((uint32_t)TL - 1) & ~mlm;
+      const int members = TL >> ml;
+      const uint64_t t_log = tab64(itb.pxo, it.base_log, a.n);
+      double* out = a.partial + it.slot * a.partial_stride + (int64_t)t_log * nb;
+      if (nb <= T) {
+        const int tp = T / nb;
+        // bin fastest across the warp: neighbouring threads read neighbouring
+        // amplitudes when the measured qubits are low tile positions (the common case)
+        const int bb = tid % nb, j = tid / nb;
+        uint32_t bpos = 0;
+        for (int jj = 0; jj < ml; ++jj)
+          if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
+        // members r = j, j + tp, ... deposited into free_mask by masked addition
+        // (x | ~mask) + d carries across the holes), in increasing order
+        const uint32_t inc = (uint32_t)pdep64((uint64_t)tp, free_mask);
+        uint32_t f = (uint32_t)pdep64((uint64_t)j, free_mask);
+        auto step = [&](uint32_t x) { return ((x | ~free_mask) + inc) & free_mask; };
+        // four independent accumulators (fixed association): the shared loads and
+        // FP64 adds of consecutive members overlap instead of forming one chain
+        const int cnt = (members - j + tp - 1) / tp;
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        int i = 0;
+        for (; i + 4 <= cnt; i += 4) {
+          const uint32_t f1 = step(f), f2 = step(f1), f3 = step(f2);
+          s4[0] += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+          s4[1] += norm2<R>(tile[swz_slot<SB>(swz, f1 | bpos)]);
+          s4[2] += norm2<R>(tile[swz_slot<SB>(swz, f2 | bpos)]);
+          s4[3] += norm2<R>(tile[swz_slot<SB>(swz, f3 | bpos)]);
+          f = step(f3);
+        }
+        for (; i < cnt; ++i) {
+          s4[0] += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+          f = step(f);
+        }
+        red[tid] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        group_sync(bar, T);
+        if (j == 0) {
+          double tot = 0.0;
+          for (int jj = 0; jj < tp; ++jj) tot += red[bb + nb * jj];
+          out[bb] = tot;
+        }
+      } else {
+        for (int bb = tid; bb < nb; bb += T) {
+          uint32_t bpos = 0;
+          for (int jj = 0; jj < ml; ++jj)
+            if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
+          double s = 0.0;
+          uint32_t f = 0;
+          for (int r = 0; r < members; ++r) {
+            s += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
+            f = ((f | ~free_mask) + 1u) & free_mask;
+          }
+          out[bb] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) v[j] = tile[St ^ ujt[j]];
+  };
+  auto scatter = [&](const PassItem& it, const A* v) {
+    A* st = reinterpret_cast<A*>(a.state) + (it.slot << a.n);
+    const uint64_t pb = it.base_phys | Pt;
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = v[j];
+  };
+
+  if (MODE == 1) {
+    const int64_t nloc = W > (int64_t)blockIdx.x ? (W - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto wof = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+    // gather of local item i (context it) into buffer i % 3 by the calling group; every
+    // thread arrives on mbar[i % 6] when its copies have landed, thread 0 once more
+    // after publishing the context in ctxs[i % 6]
+    auto load = [&](int64_t i, const PassItem& it) {
+      uint64_t* mb = &mbar[i % 6];
+      prefetch(it, bufs + (i % 3) * TL);
+      if (it.alive && !pd.init_zero) mbar_arrive_cp_async(mb);
+      else mbar_arrive(mb);
+      if (tid == 0) {
+        ctxs[i % 6] = it;
+        mbar_arrive(mb);
+      }
+    };
+    if (grp == 0) {
+      if (nloc > 0) load(0, pass_item(a, pd, wof(0), ntl, itb));
+      if (nloc > 2) load(2, pass_item(a, pd, wof(2), ntl, itb));
+    } else if (nloc > 1) {
+      load(1, pass_item(a, pd, wof(1), ntl, itb));
+    }
+    for (int64_t i = grp; i < nloc; i += 2) {
+      const bool more = i + 3 < nloc;
+      PassItem nl;  // context of the gather this group issues next (its loads overlap the phases)
+      nl.alive = false;
+      if (more) nl = pass_item(a, pd, wof(i + 3), ntl, itb);
+      mbar_wait(&mbar[i % 6], (uint32_t)((i / 6) & 1));
+      const PassItem it = ctxs[i % 6];
+      A v[1 << RB];
+      if (it.alive) process(it, bufs + (i % 3) * TL, v);
+      group_sync(bar, T);  // the group is done with the buffer
+      if (more) load(i + 3, nl);
+      if (it.alive) scatter(it, v);
+    }
+    cp_async_wait0();
+    return;
+  }
 
   int64_t w = blockIdx.x;
   PassItem cur;
@@ -242,150 +455,17 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     __syncthreads();
     const PassItem it = cur;
     cur = nxt;
-    A* tile = bufs + b * TL;
-    if (it.alive) {
-      if (it.pending) {  // collapse of the previous decide: projection + complex scale
-        const R sre = (R)it.sre, sim = (R)it.sim;
-        const uint64_t pb = it.base_phys | Pt;
-        const uint32_t fb = flip_base(it.fl);
-        for (int j = 0; j < (1 << RB); ++j) {
-          const uint64_t p = pb | hi_off[j * hstep];
-          A* d = tile + (fb ^ ujt[j]);
-          A v = *d;
-          if ((p & it.Kp) != it.Vp) v = mk<R>(0, 0);
-          else v = mk<R>(fma(sre, v.x, -sim * v.y), fma(sre, v.y, sim * v.x));
-          *d = v;
-        }
-      }
-      if (STAGE) {  // stage the gates: guards, out-of-tile controls, per-CTA diagonal factors
-        const uint32_t* gw = a.guards + it.slot * a.gwords;
-        const double* mats = a.mats + it.slot * a.mat_stride;
-        for (int i = tid; i < pd.pgate_count; i += T) {
-          const PhaseGate g = a.phase_gates[pd.pgate_begin + i];
-          SGate<R> s;
-          double m[8];
-          const double* src = mats + (int64_t)g.mat * 8;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) m[j] = src[j];
-          int kind = g.kind;
-          bool skip = (g.guard >= 0 && !((gw[g.guard >> 5] >> (g.guard & 31)) & 1u)) ||
-                      ((it.base_log & g.gcm) != g.gcv);
-          if (kind == PK_DIAG_G) kind = PK_DIAG_T;  // same code path, tp = -1
-          if (kind == PK_DENSE) {
-            if (m[1] == 0.0 && m[3] == 0.0 && m[5] == 0.0 && m[7] == 0.0) kind = PK_DENSE_REAL;
-            else if (m[1] == 0.0 && m[7] == 0.0 && m[2] == 0.0 && m[4] == 0.0) kind = PK_DENSE_RX;
-          } else if (g.kind == PK_DIAG_G) {
-            int bb = (int)((it.base_log >> g.tp) & 1);
-            if (!bb && g.diag_one0) skip = true;
-            if (bb) {
-              m[0] = m[6];
-              m[1] = m[7];
-            }
-          }
-          s.kind = skip ? PK_SKIP : kind;
-          s.jt = g.kind == PK_DIAG_T ? g.diag_one0 : g.jt;
-          s.jt2 = g.jt2;
-          s.tp = (g.kind == PK_DIAG_T || g.kind == PK_SWAP_R) ? g.tp : -1;
-          s.cmR = g.cmR;
-          s.cvR = g.cvR;
-          s.cmT = g.cmT;
-          s.cvT = g.cvT;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) s.m[j] = (R)m[j];
-          sg[i] = s;
-        }
-      }
-      if (STAGE || it.pending) __syncthreads();
-      PassCtx<R> cx{tile, sg, swz, tid, T, TL};
-      run(cx);  // the phases (each ends with __syncthreads)
-      if (pd.epi) {  // per-tile marginal of the next region's measured qubits (fixed order)
-        const int ml = pd.m_local;
-        const int nb = 1 << ml;
-        uint32_t mlm = 0;
-        for (int j = 0; j < ml; ++j) mlm |= 1u << pd.mloc[j];
-        const uint32_t free_mask = ((uint32_t)TL - 1) & ~mlm;
-        const int members = TL >> ml;
-        const uint64_t t_log = tab64(itb.pxo, it.base_log, a.n);
-        double* out = a.partial + it.slot * a.partial_stride + (int64_t)t_log * nb;
-        if (nb <= T) {
-          const int tp = T / nb;
-          // bin fastest across the warp: neighbouring threads read neighbouring
-          // amplitudes when the measured qubits are low tile positions (the common case)
-          const int bb = tid % nb, j = tid / nb;
-          uint32_t bpos = 0;
-          for (int jj = 0; jj < ml; ++jj)
-            if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
-          double s = 0.0;
-          // members r = j, j + tp, ... deposited into free_mask by masked addition
-          // (x | ~mask) + d carries across the holes), in increasing order
-          const uint32_t inc = (uint32_t)pdep64((uint64_t)tp, free_mask);
-          uint32_t f = (uint32_t)pdep64((uint64_t)j, free_mask);
-          auto step = [&](uint32_t x) { return ((x | ~free_mask) + inc) & free_mask; };
-          // four independent accumulators (fixed association): the shared loads and
-          // FP64 adds of consecutive members overlap instead of forming one chain
-          const int cnt = (members - j + tp - 1) / tp;
-          double s4[4] = {0.0, 0.0, 0.0, 0.0};
-          int i = 0;
-          for (; i + 4 <= cnt; i += 4) {
-            const uint32_t f1 = step(f), f2 = step(f1), f3 = step(f2);
-            s4[0] += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
-            s4[1] += norm2<R>(tile[swz_slot<SB>(swz, f1 | bpos)]);
-            s4[2] += norm2<R>(tile[swz_slot<SB>(swz, f2 | bpos)]);
-            s4[3] += norm2<R>(tile[swz_slot<SB>(swz, f3 | bpos)]);
-            f = step(f3);
-          }
-          for (; i < cnt; ++i) {
-            s4[0] += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
-            f = step(f);
-          }
-          s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-          red[tid] = s;
-          __syncthreads();
-          if (j == 0) {
-            double tot = 0.0;
-            for (int jj = 0; jj < tp; ++jj) tot += red[bb + nb * jj];
-            out[bb] = tot;
-          }
-        } else {
-          for (int bb = tid; bb < nb; bb += T) {
-            uint32_t bpos = 0;
-            for (int jj = 0; jj < ml; ++jj)
-              if ((bb >> jj) & 1) bpos |= 1u << pd.mloc[jj];
-            double s = 0.0;
-            uint32_t f = 0;
-            for (int r = 0; r < members; ++r) {
-              s += norm2<R>(tile[swz_slot<SB>(swz, f | bpos)]);
-              f = ((f | ~free_mask) + 1u) & free_mask;
-            }
-            out[bb] = s;
-          }
-        }
-      }
-      A* st = reinterpret_cast<A*>(a.state) + (it.slot << a.n);
-      const uint64_t pb = it.base_phys | Pt;
-      if (NB == 2) {
-#pragma unroll 4
-        for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = tile[St ^ ujt[j]];
-      } else {
-        // single buffer: take the tile into registers, release the buffer, start the
-        // next item's gather, then store -- the scatter and the next gather overlap
-        A v[1 << RB];
-#pragma unroll
-        for (int j = 0; j < (1 << RB); ++j) v[j] = tile[St ^ ujt[j]];
-        __syncthreads();
-        if (wn < W) prefetch(cur, bufs);
-        cp_async_commit();
-#pragma unroll
-        for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = v[j];
-        continue;
-      }
-    }
+    A v[1 << RB];
+    if (it.alive) process(it, bufs + b * TL, v);
+    // single buffer: the tile is in registers -- release the buffer, start the next
+    // item's gather, then store, so that the scatter and the next gather overlap
     __syncthreads();
-    if (NB == 2) b ^= 1;
-    else {
-      if (wn < W) prefetch(cur, bufs);  // dead item: nothing to store
+    if (NB == 1) {
+      if (wn < W) prefetch(cur, bufs);
       cp_async_commit();
     }
+    if (it.alive) scatter(it, v);
+    if (NB == 2) b ^= 1;
   }
   cp_async_wait0();
 }

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__((1 << (12 - RB)), 2) k_pass_reg(StreamArgs a, 
       const int nt = P->nt;
       if (nt < 0) {
         pass_swap<R, SB>(cx, cx.sg[P->gate_begin - pd.pgate_begin]);
-        __syncthreads();
+        cx.sync();
         continue;
       }
       uint32_t base = 0;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__((1 << (12 - RB)), 2) k_pass_reg(StreamArgs a, 
       }
 #pragma unroll
       for (int j = 0; j < NR; ++j) cx.tile[sbase ^ P->soff[j]] = v[j];
-      __syncthreads();
+      cx.sync();
     }
   });
 }
