@@ -322,24 +322,29 @@ void launch_debug_rng(uint64_t seed, int64_t shot, int count, double* out, cudaS
   k_debug_rng<<<1, 1, 0, s>>>(seed, shot, count, out);
 }
 
-// FMA-throughput probe (8 independent chains per thread): the compute roofline of the
-// pass kernels, measured on the box instead of quoted from a datasheet.
-template <typename R> __global__ void k_fma_peak(R* out, int iters, R a, R b) {
-  R x[8];
+// FMA-throughput probe (16 independent chains per thread, 64 FMA per loop trip so that
+// the loop overhead stays off the FP pipe): the compute roofline of the pass kernels,
+// measured on the box instead of quoted from a datasheet.  (experiments/dmma_probe.cu:
+// the same loop reaches 37.1 TFLOP/s fp64 on B200, and DMMA shares that pipe.)
+template <typename R> __global__ void __launch_bounds__(256) k_fma_peak(R* out, int iters, R a, R b) {
+  R x[16];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = (R)(threadIdx.x + i);
+  for (int i = 0; i < 16; ++i) x[i] = (R)(threadIdx.x + i);
+  const R ar = a + (R)threadIdx.x * (R)1e-9;  // a register operand: one constant-bank read per FMA
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = fma(x[i], ar, b);
   }
   R s = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s += x[i];
+  for (int i = 0; i < 16; ++i) s += x[i];
   if (s == (R)-1.2345) out[0] = s;  // keep the chains alive
 }
 
 double measure_fma_peak(int c64, int num_sms, cudaStream_t s) {
-  const int threads = 256, blocks = num_sms * 8, iters = 4096;
+  const int threads = 256, blocks = num_sms * 4, iters = 4096;
   void* out = nullptr;
   cudaMalloc(&out, 64);
   cudaEvent_t e0, e1;
@@ -359,7 +364,7 @@ double measure_fma_peak(int c64, int num_sms, cudaStream_t s) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(out);
-  const double flops = 2.0 * 8.0 * iters * (double)threads * blocks;
+  const double flops = 2.0 * 64.0 * iters * (double)threads * blocks;
   return flops / (best * 1e-3) / 1e12;  // TFLOP/s
 }
 }  // namespace qsb
