@@ -116,10 +116,13 @@ def cfg5(args):
     _, k = workloads.rdc_circuit(n=30, depth=20, every=10, seed=34)
     b = ir.bind(k, [])
     for fuse in (False, True):
-        t0 = time.perf_counter()
-        store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(1234, 0), 3,
-                                                 backend=sliced.GpuSliceBackend(fuse=fuse))
-        dt = time.perf_counter() - t0
+        for rep in range(2):  # the first run pays slice allocation and plan construction
+            t0 = time.perf_counter()
+            store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(1234, 0), 3,
+                                                     backend=sliced.GpuSliceBackend(fuse=fuse))
+            dt = time.perf_counter() - t0
+            if rep == 0:
+                del st
         _emit({"config": f"cfg5 sliced RDC30 depth 20, 3 global qubits emulated (8 slices of 2^27), "
                          f"{'fused' if fuse else 'per-op'} slice gates",
                "trajectory_s": dt, "exchanges": st.exchanges, "key": store.key()})
