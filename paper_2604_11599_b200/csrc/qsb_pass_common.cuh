@@ -101,23 +101,49 @@ __device__ __forceinline__ uint32_t tab32(const uint32_t* t, uint64_t x, int nbi
   return r;
 }
 
+// the per-state part of an item's context (one TrajCtl read)
+struct SlotCtx {
+  int64_t idx;  // active-list index (w >> ntl)
+  int64_t slot;
+  uint64_t F, Kp, Vp;
+  double sre, sim;
+  bool alive, pending;
+};
+
+__device__ __forceinline__ SlotCtx slot_ctx(const StreamArgs& a, const PassDesc& pd, int64_t idx) {
+  SlotCtx s;
+  s.idx = idx;
+  s.slot = a.active ? a.active[idx] : idx;  // representative slots only (history dedup)
+  const TrajCtl* c = a.ctl + s.slot;
+  s.alive = c->status == 0;
+  s.F = c->frame & ~pd.clear_before;
+  s.pending = pd.prologue && c->pending;
+  s.Kp = c->kmask;
+  s.Vp = c->kval;
+  s.sre = c->sre;
+  s.sim = c->sim;
+  return s;
+}
+
+__device__ __forceinline__ PassItem item_of(const SlotCtx& s, const PassDesc& pd, uint64_t tile, int ntl, int n,
+                                            const ItemTables& tb) {
+  PassItem it;
+  it.slot = s.slot;
+  it.alive = s.alive;
+  it.pending = s.pending;
+  it.Kp = s.Kp;
+  it.Vp = s.Vp;
+  it.sre = s.sre;
+  it.sim = s.sim;
+  it.base_phys = tab64(tb.pdt, tile, ntl);
+  it.base_log = it.base_phys ^ (s.F & ~pd.smask);
+  it.fl = tab32(tb.pxs, s.F, n);
+  return it;
+}
+
 __device__ __forceinline__ PassItem pass_item(const StreamArgs& a, const PassDesc& pd, int64_t w, int ntl,
                                               const ItemTables& tb) {
-  PassItem it;
-  it.slot = a.active ? a.active[w >> ntl] : (w >> ntl);  // representative slots only (history dedup)
-  const uint64_t tile = (uint64_t)w & ((1ull << ntl) - 1);
-  const TrajCtl* c = a.ctl + it.slot;
-  it.alive = c->status == 0;
-  const uint64_t F = c->frame & ~pd.clear_before;
-  it.pending = pd.prologue && c->pending;
-  it.Kp = c->kmask;
-  it.Vp = c->kval;
-  it.sre = c->sre;
-  it.sim = c->sim;
-  it.base_phys = tab64(tb.pdt, tile, ntl);
-  it.base_log = it.base_phys ^ (F & ~pd.smask);
-  it.fl = tab32(tb.pxs, F, a.n);
-  return it;
+  return item_of(slot_ctx(a, pd, w >> ntl), pd, (uint64_t)w & ((1ull << ntl) - 1), ntl, a.n, tb);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -393,8 +419,20 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   };
 
   if (MODE == 1) {
-    const int64_t nloc = W > (int64_t)blockIdx.x ? (W - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    auto wof = [&](int64_t i) { return (int64_t)blockIdx.x + i * (int64_t)gridDim.x; };
+    // a contiguous range of items per CTA: consecutive items are tiles of the same state,
+    // so the loader re-reads a TrajCtl only when the state changes (the context is then
+    // off the groups' critical path)
+    const int64_t per = (W + gridDim.x - 1) / gridDim.x;
+    const int64_t wbeg = (int64_t)blockIdx.x * per;
+    const int64_t nloc = W > wbeg ? (W - wbeg < per ? W - wbeg : per) : 0;
+    auto wof = [&](int64_t i) { return wbeg + i; };
+    SlotCtx sc;
+    sc.idx = -1;
+    auto ctx_of = [&](int64_t i) {
+      const int64_t w = wof(i);
+      if ((w >> ntl) != sc.idx) sc = slot_ctx(a, pd, w >> ntl);
+      return item_of(sc, pd, (uint64_t)w & ((1ull << ntl) - 1), ntl, a.n, itb);
+    };
     // gather of local item i (context it) into buffer i % 3 by the calling group; every
     // thread arrives on mbar[i % 6] when its copies have landed, thread 0 once more
     // after publishing the context in ctxs[i % 6]
@@ -409,22 +447,19 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
       }
     };
     if (grp == 0) {
-      if (nloc > 0) load(0, pass_item(a, pd, wof(0), ntl, itb));
-      if (nloc > 2) load(2, pass_item(a, pd, wof(2), ntl, itb));
+      if (nloc > 0) load(0, ctx_of(0));
+      if (nloc > 2) load(2, ctx_of(2));
     } else if (nloc > 1) {
-      load(1, pass_item(a, pd, wof(1), ntl, itb));
+      load(1, ctx_of(1));
     }
     for (int64_t i = grp; i < nloc; i += 2) {
       const bool more = i + 3 < nloc;
-      PassItem nl;  // context of the gather this group issues next (its loads overlap the phases)
-      nl.alive = false;
-      if (more) nl = pass_item(a, pd, wof(i + 3), ntl, itb);
       mbar_wait(&mbar[i % 6], (uint32_t)((i / 6) & 1));
       const PassItem it = ctxs[i % 6];
       A v[1 << RB];
       if (it.alive) process(it, bufs + (i % 3) * TL, v);
       group_sync(bar, T);  // the group is done with the buffer
-      if (more) load(i + 3, nl);
+      if (more) load(i + 3, ctx_of(i + 3));
       if (it.alive) scatter(it, v);
     }
     cp_async_wait0();

@@ -41,3 +41,33 @@ def test_reg_bits_rejected():
 
 def test_ctypes_signature():
     assert _lib._SIGS["qsb_jit_selftest"][1][6] is ctypes.c_int32
+
+
+def _fusion_stats(kernel, precision, reg_bits):
+    lib = _lib.load()
+    recs = sim.tape_records(kernel)
+    nbits = sum(int(w) for _, w in kernel.classical_layout)
+    nparams = sum(p.count for p in kernel.param_layout)
+    out = np.zeros(6, dtype=np.float64)
+    _lib.check(lib.qsb_fusion_stats(_lib.ptr(recs), len(recs), int(kernel.qubit_count), nbits, nparams, precision,
+                                    reg_bits, _lib.ptr(out)))
+    return out
+
+
+@pytest.mark.parametrize("precision,reg_bits", [(_lib.C128, 4), (_lib.C64, 5), (_lib.C128, 3)])
+def test_phase_fusion_host_check(precision, reg_bits):
+    """Register-phase 2x2 / 4x4 fusion (qsb_plan.cpp fuse_phase): every fused phase of
+    the DYN20 brick and of a random dynamic circuit reproduces its gates on random
+    register vectors (host check, 0 failures), and the fused kernels execute fewer
+    FP operations (DYN20: the u gates around each cx fold into one 4x4)."""
+    _, k = workloads.dyn_circuit()
+    st = _fusion_stats(k, precision, reg_bits)
+    assert st[3] == 0, st
+    assert st[1] > 0 and st[2] >= 2 * st[1], st
+    assert st[5] < 0.85 * st[4], st
+    _, k2 = workloads.rdc_circuit(n=18, depth=30, every=10, seed=5)
+    st2 = _fusion_stats(k2, precision, reg_bits)
+    assert st2[3] == 0 and st2[5] <= st2[4], st2
+    k3 = workloads.random_static(14, 300, seed=9, nparams=2, max_controls=2)
+    st3 = _fusion_stats(k3, precision, reg_bits)
+    assert st3[3] == 0 and st3[5] <= st3[4], st3
