@@ -454,7 +454,10 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     }
     for (int64_t i = grp; i < nloc; i += 2) {
       const bool more = i + 3 < nloc;
-      mbar_wait(&mbar[i % 6], (uint32_t)((i / 6) & 1));
+      // one warp polls the mbarrier; the rest of the group sleeps in the named barrier
+      // instead of spinning on try_wait (which steals issue slots from the other group)
+      if (tid < 32) mbar_wait(&mbar[i % 6], (uint32_t)((i / 6) & 1));
+      group_sync(bar, T);
       const PassItem it = ctxs[i % 6];
       A v[1 << RB];
       if (it.alive) process(it, bufs + (i % 3) * TL, v);
