@@ -224,15 +224,22 @@ void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr) {
 }
 
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
-                const PhaseDesc& ph, int sb, const std::vector<FuseItem>& items, int cf0) {
+                const PhaseDesc& ph, int sb, const std::vector<FuseItem>& items, int cf0, bool direct = false) {
   const int nr = 1 << P.rb;  // amplitudes per thread
-  o << "__device__ __noinline__ void ph" << ph_index
-    << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
-       "const int tid) {\n";
+  if (direct) {  // last phase of a DIRECT pass (qsb_pass_common.cuh): inlined, stores to HBM
+    o << "template <typename MID> __device__ __forceinline__ void phL"
+      << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
+         "const int tid, A* __restrict__ dst, const uint64_t* __restrict__ hi_off, MID mid) {\n";
+  } else {
+    o << "__device__ __noinline__ void ph" << ph_index
+      << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
+         "const int tid) {\n";
+  }
   o << "  const uint32_t base = 0u";
   for (int i = 0; i < ph.nt; ++i) o << " | ((((uint32_t)tid >> " << i << ") & 1u) << " << (int)ph.tpos[i] << ")";
   o << ";\n  const uint32_t sb = base ^ swz[base >> " << sb << "];\n";
   for (int j = 0; j < nr; ++j) o << "  A v" << j << " = tile[sb ^ " << ph.soff[j] << "u];\n";
+  if (direct) o << "  mid();\n";
   int cf = cf0;
   for (const FuseItem& item : items) {
     if (item.gate < 0) {
@@ -317,7 +324,33 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
     if (need_skip) o << "  }\n";
     o << "  }\n";
   }
-  for (int j = 0; j < nr; ++j) o << "  tile[sb ^ " << ph.soff[j] << "u] = v" << j << ";\n";
+  if (direct) {
+    // HBM offset of register j: pdep over the tile qubits is linear over disjoint bits, so
+    // it is the thread's part (hi_off table) OR a compile-time constant per register
+    uint32_t tmask = 0;
+    for (int i = 0; i < ph.nt; ++i) tmask |= 1u << ph.tpos[i];
+    int rpos[kMaxRegBits], nrb = 0;
+    for (int p = 0; p < pd.k; ++p)
+      if (!(tmask >> p & 1)) rpos[nrb++] = p;
+    o << "  const uint64_t tof = (uint64_t)(base & " << ((1u << pd.lowq) - 1) << "u) | hi_off[base >> " << pd.lowq
+      << "];\n";
+    for (int j = 0; j < nr; ++j) {
+      uint64_t l = 0;
+      for (int b = 0; b < nrb; ++b)
+        if (j >> b & 1) l |= 1ull << rpos[b];
+      // tile element l -> qubit offsets (local bit p <-> p-th qubit of S)
+      uint64_t off = 0;
+      int p = 0;
+      for (int q = 0; q < 64 && p < pd.k; ++q)
+        if (pd.smask >> q & 1) {
+          if (l >> p & 1) off |= 1ull << q;
+          ++p;
+        }
+      o << "  dst[tof | " << off << "ull] = v" << j << ";\n";
+    }
+  } else {
+    for (int j = 0; j < nr; ++j) o << "  tile[sb ^ " << ph.soff[j] << "u] = v" << j << ";\n";
+  }
   o << "}\n";
 }
 
@@ -347,6 +380,24 @@ int jit_pass_mode(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
   if (c64 || !(e && *e && atoi(e) == 1)) return 0;
   const size_t sm = pass_reg_smem(c64, P.passes[pass], P.rb, t.n, pass_needs_stage(t, P, pass), 1);
   return sm <= 227 * 1024 ? 1 : 0;
+}
+
+// DIRECT last phase (qsb_pass_common.cuh): complex128 MODE 0 passes without an epilogue
+// whose last phase is a register phase with coalesced stores.  Opt-in ($QSB_LAST_DIRECT=1):
+// measured on B200 it lifts the streaming probe (4.46 -> 4.75 TB/s) but slows VQE24 c128
+// (186 -> 160 points/s); no DYN20 pass qualifies (its last phases hold qubits 0-3 in
+// registers, which would make the stores uncoalesced).
+bool jit_pass_direct(const TapeInfo& t, const StreamPlan& P, int pass, int c64, int mode) {
+  const char* e = getenv("QSB_LAST_DIRECT");
+  if (!(e && *e && atoi(e) == 1)) return false;
+  const PassDesc& pd = P.passes[pass];
+  if (c64 || mode != 0 || pd.epi || pd.phase_count < 1) return false;
+  const PhaseDesc& ph = P.phases[pd.phase_begin + pd.phase_count - 1];
+  if (ph.nt < 3) return false;
+  // coalesced stores: lanes 0..7 of a warp must cover 8 consecutive amplitudes (128 B)
+  for (int i = 0; i < 3; ++i)
+    if (ph.tpos[i] != i) return false;
+  return true;
 }
 
 std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64, bool fuse) {
@@ -402,26 +453,31 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
     }
     o << "};\n";
   }
+  const int mode = jit_pass_mode(t, P, pass, c64);
+  const bool direct = jit_pass_direct(t, P, pass, c64, mode);
   for (int i = 0; i < pd.phase_count; ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
-    if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb, items[i], cf0[i]);
+    if (ph.nt >= 0) emit_phase(o, t, P, pd, i, ph, sb, items[i], cf0[i], direct && i == pd.phase_count - 1);
   }
   const bool stage = pass_needs_stage(t, P, pass);
-  const int mode = jit_pass_mode(t, P, pass, c64);
   const int threads = pass_groups(mode) << (pd.k - P.rb);
+  if (direct)
+    o << "struct LastPhase {\n  template <typename MID> __device__ void operator()(const qsb::PassCtx<R>& cx, A* dst, "
+         "const uint64_t* hi_off, MID mid) const {\n    phL(cx.tile, cx.swz, cx.sg, cx.tid, dst, hi_off, mid);\n  }\n};\n";
   const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
   o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
     << (mode == 1 ? 1 : (mb && *mb ? atoi(mb) : 2)) << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-  o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false") << ", " << mode
-    << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
-  for (int i = 0; i < pd.phase_count; ++i) {
+  o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false") << ", " << mode << ", "
+    << (direct ? "true" : "false") << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
+  for (int i = 0; i < pd.phase_count - (direct ? 1 : 0); ++i) {
     const PhaseDesc& ph = P.phases[pd.phase_begin + i];
     if (ph.nt >= 0) o << "    ph" << i << "(cx.tile, cx.swz, cx.sg, cx.tid);\n";
     else o << "    qsb::pass_swap<R, " << sb << ">(cx, cx.sg[" << (ph.gate_begin - pd.pgate_begin) << "]);\n";
     o << "    cx.sync();\n";
   }
-  o << "  });\n}\n";
+  if (direct) o << "  }, LastPhase());\n}\n";
+  else o << "  });\n}\n";
   return o.str();
 }
 

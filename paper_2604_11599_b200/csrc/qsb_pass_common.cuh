@@ -209,9 +209,20 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
 // false when none of their phases reads the staged gates (literal matrices from the
 // constant bank, no per-item decisions), which removes a global-load round trip and a
 // barrier from every item.
-template <typename R, int RB, bool STAGE = true, int MODE = 0, typename PhaseRunner>
+// DIRECT (NVRTC complex128 passes without an epilogue, MODE 0): `run` executes every
+// phase but the last; `run_last(cx, dst, hi_off, mid)` loads the last phase's registers
+// from the tile, calls mid() -- which releases the buffer and issues the next item's
+// gather -- and then computes and stores its registers straight to HBM, so the gather
+// overlaps the last phase's arithmetic and the tile makes one shared-memory round trip
+// less.
+struct NoLastPhase {
+  template <typename... T> __device__ void operator()(T&&...) const {}
+};
+
+template <typename R, int RB, bool STAGE = true, int MODE = 0, bool DIRECT = false, typename PhaseRunner,
+          typename LastRunner = NoLastPhase>
 __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassDesc& pd, unsigned char* smem_raw,
-                                                PhaseRunner run) {
+                                                PhaseRunner run, LastRunner run_last = LastRunner()) {
   using A = typename Amp<R>::T;
   constexpr int SB = sizeof(R) == 8 ? 3 : 4;
   constexpr int G = MODE == 1 ? 2 : 1;  // thread groups
@@ -347,6 +358,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     if (STAGE || it.pending) group_sync(bar, T);
     PassCtx<R> cx{tile, sg, swz, tid, T, TL, bar};
     run(cx);  // the phases (each ends with cx.sync())
+    if (DIRECT) return;
     if (pd.epi) {  // per-tile marginal of the next region's measured qubits (fixed order)
       const int ml = pd.m_local;
       const int nb = 1 << ml;
@@ -493,6 +505,23 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     __syncthreads();
     const PassItem it = cur;
     cur = nxt;
+    if (DIRECT && NB == 1) {
+      auto mid = [&]() {
+        __syncthreads();  // every thread holds its last-phase registers: the buffer is free
+        if (wn < W) prefetch(cur, bufs);
+        cp_async_commit();
+      };
+      if (it.alive) {
+        A dummy[1];
+        process(it, bufs, dummy);
+        PassCtx<R> cx{bufs, sg, swz, tid, T, TL, bar};
+        A* dst = reinterpret_cast<A*>(a.state) + (it.slot << a.n) + it.base_phys;
+        run_last(cx, dst, hi_off, mid);
+      } else {
+        mid();
+      }
+      continue;
+    }
     A v[1 << RB];
     if (it.alive) process(it, bufs + b * TL, v);
     // single buffer: the tile is in registers -- release the buffer, start the next
