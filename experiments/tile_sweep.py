@@ -8,8 +8,9 @@ b = ir.bind(k, [])
 ctx = _lib.context()
 ctx.set_option("tile_qubits", tile)
 ctx.set_option("reg_bits", int(os.environ.get("RB", "4")))
+ctx.set_option("low_qubits", int(os.environ.get("LOWQ", "0")))
 B = 2048
 for rep in range(3):
     sim.sample_words(b, B, 1234, shot_begin=rep * B, precision=prec)
     st = sim.last_stats()
-print(f"rb {os.environ.get('RB', 4)} tile {tile} {prec} minblocks {os.environ.get('QSB_JIT_MINBLOCKS')} passes/step {st['passes']} pass_ms {st['pass_ms']:.1f} total_ms {st['total_ms']:.1f} shots/s {B / st['total_ms'] * 1e3:.0f}")
+print(f"lowq {os.environ.get('LOWQ', 0)} rb {os.environ.get('RB', 4)} tile {tile} {prec} minblocks {os.environ.get('QSB_JIT_MINBLOCKS')} passes/step {st['passes']} pass_ms {st['pass_ms']:.1f} total_ms {st['total_ms']:.1f} shots/s {B / st['total_ms'] * 1e3:.0f}")

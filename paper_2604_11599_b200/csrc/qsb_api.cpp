@@ -118,7 +118,10 @@ int tile_qubits(qsb_ctx ctx, int c64) {
   if (ctx->opt_tile > 0) return (int)std::min<int64_t>(ctx->opt_tile, kMaxTile);
   return 12;  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA
 }
-int low_qubits(int c64) { return c64 ? 5 : 4; }  // 256-byte contiguous runs
+// contiguous low qubits of every tile: 256-byte runs by default (option low_qubits
+// overrides; shorter runs let a tile cover more qubits of a light cone)
+int64_t g_opt_lowq = 0;
+int low_qubits(int c64) { return g_opt_lowq > 0 ? (int)g_opt_lowq : (c64 ? 5 : 4); }
 
 // Blocking copy ordered on the context's stream.  ctx->stream is non-blocking, so a plain
 // cudaMemcpy (legacy stream) neither waits for work queued on it nor -- for pageable
@@ -150,18 +153,17 @@ int upload_tape_device(qsb_tape tp) {
 
 int reg_bits(qsb_ctx ctx) { return (int)ctx->opt_reg_bits; }  // amplitudes per thread = 2^reg_bits
 
-int get_plan(qsb_tape tp, int k, int lowq, int rb, PlanDev** out) {
-  const int c64 = lowq == 5 ? 1 : 0;
+int get_plan(qsb_tape tp, int c64, int k, int lowq, int rb, PlanDev** out) {
   const bool want_jit = tp->ctx->opt_jit && tp->info.n >= tp->ctx->opt_jit_min;
   const bool fuse = tp->ctx->opt_fuse != 0;
-  int key = (((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0)) * 2 + (fuse ? 1 : 0);
+  int key = ((((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0)) * 2 + (fuse ? 1 : 0)) * 2 + c64;
   auto it = tp->plans.find(key);
   if (it != tp->plans.end()) {
     *out = it->second.get();
     return QSB_OK;
   }
   auto pd = std::make_unique<PlanDev>();
-  std::string e = build_stream_plan(tp->info, k, lowq, rb, swizzle_bits(lowq == 5), pd->plan);
+  std::string e = build_stream_plan(tp->info, k, lowq, rb, swizzle_bits(c64), pd->plan);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   StreamPlan& P = pd->plan;
   QSB_CUDA(pd->gates.ensure(std::max<size_t>(1, P.gates.size()) * sizeof(PassGate)));
@@ -529,7 +531,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit") ctx->opt_jit = value;        // NVRTC per-pass kernels (1) or generic kernel (0)
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
-  else if (k == "fuse") ctx->opt_fuse = value;      // register-phase gate fusion in the NVRTC kernels    // branch-history deduplication of trajectories
+  else if (k == "fuse") ctx->opt_fuse = value;
+  else if (k == "low_qubits") g_opt_lowq = value;   // 0: default (4 complex128, 5 complex64)      // register-phase gate fusion in the NVRTC kernels    // branch-history deduplication of trajectories
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
     ctx->opt_reg_bits = value;
@@ -1090,7 +1093,7 @@ int sample_traj_impl(qsb_tape tp, int32_t precision, const double* params, uint6
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+    rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
     if (rc) return rc;
     int64_t B = pick_batch(ctx, t, pd->plan, c64, shot_count);
     QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
@@ -1219,7 +1222,7 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+    rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
     if (rc) return rc;
     QSB_CUDA(ctx->state.ensure(amp_bytes(c64) << t.n));
     StreamRun r{tp, pd, c64, 1, ctx->state.p, mats, mstride, seed, shot, d_pre, npredrawn, 0, d_trace, max_trace,
@@ -1280,7 +1283,7 @@ int32_t qsb_apply_tape(qsb_tape tp, const double* params, qsb_state st) {
   rc = prepare_mats(tp, d_params, 1, &mats, &mstride);
   if (rc) return rc;
   PlanDev* pd;
-  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   StreamRun r{tp, pd, c64, 1, st->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
   r.in_place = true;
@@ -1336,7 +1339,7 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
     return QSB_OK;
   }
   PlanDev* pd;
-  rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   StreamRun r{tp, pd, c64, 1, out->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
   rc = run_stream(ctx, r);
@@ -1468,7 +1471,7 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   ctx->run_physical = false;
   RunTimer timer(ctx);
   PlanDev* pd;
-  int rc = get_plan(tp, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  int rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   int64_t B = pick_batch(ctx, t, pd->plan, c64, npoints);
   QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
