@@ -18,7 +18,7 @@ k = k[1] if isinstance(k, tuple) else k
 H = workloads.vqe_hamiltonian()
 pts = workloads.vqe_points(32)
 for prec in ("c128", "c64"):
-    sim.observe(k, H, pts[:4], precision=prec)
+    sim.observe(k, H, pts, precision=prec)
     e = sim.observe(k, H, pts, precision=prec)
     st = sim.last_stats()
     print(f"lowq {lowq} VQE24 {prec} 32 points device_ms {st['total_ms']:.1f} E0 {e[0]:.15f}")

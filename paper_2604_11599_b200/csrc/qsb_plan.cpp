@@ -244,6 +244,7 @@ struct Planner {
   int k, lowq, rb;
   int swz_bits_ = 3;
   bool pair_aware_ = getenv("QSB_PAIR_AWARE") ? atoi(getenv("QSB_PAIR_AWARE")) != 0 : true;
+  bool phase_search_ = getenv("QSB_PHASE_SEARCH") ? atoi(getenv("QSB_PHASE_SEARCH")) != 0 : false;
   StreamPlan& P;
   std::vector<RegionBuild> regions;
 
@@ -283,6 +284,60 @@ struct Planner {
       }
       uint32_t R = 0, blocked = 0;
       std::vector<int> take, rest;
+      if (phase_search_ && k > rb) {
+        // choose the register set R (rb of the k tile positions, containing the target
+        // of the first remaining non-diagonal gate) under which the in-order scan absorbs
+        // the most gates -- fewer phases, i.e. fewer shared-memory round trips per pass;
+        // ties prefer two-qubit gates with both qubits in R (register controls, 4x4 fusion)
+        int first_t = -1;
+        for (int gi : rem) {
+          const PassGate& g = P.gates[gi];
+          if (g.gclass == GC_DENSE || g.gclass == GC_XPERM || g.gclass == GC_ANTI) {
+            first_t = g.lt;
+            break;
+          }
+        }
+        double best = -1.0;
+        uint32_t bestR = 0;
+        const uint32_t full = (k >= 32) ? ~0u : ((1u << k) - 1);
+        for (uint32_t c = 0; c <= full; ++c) {
+          if (popc(c) != rb || (first_t >= 0 && !(c >> first_t & 1))) continue;
+          uint32_t bl = 0;
+          double score = 0;
+          for (int gi : rem) {
+            const PassGate& g = P.gates[gi];
+            uint32_t touched = g.lcm;
+            if (g.gclass != GC_DIAG_GLOBAL) touched |= 1u << g.lt;
+            if (g.gclass == GC_SWAP) touched |= 1u << g.lt2;
+            const bool nd = g.gclass == GC_DENSE || g.gclass == GC_XPERM || g.gclass == GC_ANTI;
+            if ((touched & bl) || g.gclass == GC_SWAP || (nd && !(c >> g.lt & 1))) {
+              bl |= touched;
+              continue;
+            }
+            // a control on a thread position costs per-pair selects and blocks fusion
+            score += (g.lcm & ~c) ? 0.7 : 1.0;
+          }
+          if (score > best) {
+            best = score;
+            bestR = c;
+          }
+          if (first_t < 0) break;  // diagonal-only remainder: any R absorbs everything
+        }
+        R = bestR;
+        for (const int& gi : rem) {
+          const PassGate& g = P.gates[gi];
+          uint32_t touched = g.lcm;
+          if (g.gclass != GC_DIAG_GLOBAL) touched |= 1u << g.lt;
+          if (g.gclass == GC_SWAP) touched |= 1u << g.lt2;
+          const bool nd = g.gclass == GC_DENSE || g.gclass == GC_XPERM || g.gclass == GC_ANTI;
+          if ((touched & blocked) || g.gclass == GC_SWAP || (nd && !(R >> g.lt & 1))) {
+            rest.push_back(gi);
+            blocked |= touched;
+          } else {
+            take.push_back(gi);
+          }
+        }
+      } else
       for (const int& gi : rem) {
         const PassGate& g = P.gates[gi];
         uint32_t touched = g.lcm;
