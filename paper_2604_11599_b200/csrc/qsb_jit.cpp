@@ -152,6 +152,78 @@ __device__ __forceinline__ void G_DIAG(A& a0, A& a1, const R* m) {
 }
 )";
 
+// complex64: the same helpers on packed FP32 pairs (fma.rn.f32x2 / mul.rn.f32x2).  Each
+// lane runs exactly the scalar chain above (same terms, same order: the re lane is the
+// scalar re chain, the im lane the scalar im chain), so results are bit-identical to the
+// scalar helpers and to the generic kernel, with half the FP32 instructions.
+const char* kPackedHelpers = R"(
+__device__ __forceinline__ unsigned long long U(A a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ A F(unsigned long long d) { return *reinterpret_cast<A*>(&d); }
+__device__ __forceinline__ A ffma2(A a, A b, A c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(U(a)), "l"(U(b)), "l"(U(c)));
+  return F(d);
+}
+__device__ __forceinline__ A fmul2(A a, A b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(U(a)), "l"(U(b)));
+  return F(d);
+}
+__device__ __forceinline__ A PR(R m) { return qsb::mk<R>(m, m); }    // real part, both lanes
+__device__ __forceinline__ A PI(R m) { return qsb::mk<R>(-m, m); }   // imaginary part: (-mi, +mi)
+__device__ __forceinline__ A SW(A a) { return qsb::mk<R>(a.y, a.x); }
+__device__ __forceinline__ A CM(R mr, R mi, A a) { return ffma2(PR(mr), a, fmul2(PI(mi), SW(a))); }
+__device__ __forceinline__ A MAC2(const R* m, int o, A a0, A a1) {  // cmac2(m[o..o+1], a0, m[o+2..o+3], a1)
+  return ffma2(PR(m[o]), a0, ffma2(PI(m[o + 1]), SW(a0), ffma2(PR(m[o + 2]), a1, fmul2(PI(m[o + 3]), SW(a1)))));
+}
+__device__ __forceinline__ void G_GEN(A& a0, A& a1, const R* m) {
+  A b0 = MAC2(m, 0, a0, a1), b1 = MAC2(m, 4, a0, a1);
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_REAL(A& a0, A& a1, const R* m) {
+  A b0 = ffma2(PR(m[0]), a0, fmul2(PR(m[2]), a1));
+  A b1 = ffma2(PR(m[4]), a0, fmul2(PR(m[6]), a1));
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_RX(A& a0, A& a1, const R* m) {
+  A b0 = ffma2(PR(m[0]), a0, fmul2(PI(m[3]), SW(a1)));
+  A b1 = ffma2(PR(m[6]), a1, fmul2(PI(m[5]), SW(a0)));
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_ANTI(A& a0, A& a1, const R* m) {
+  A b0 = CM(m[2], m[3], a1);
+  A b1 = CM(m[4], m[5], a0);
+  a0 = b0; a1 = b1;
+}
+__device__ __forceinline__ void G_DIAG(A& a0, A& a1, const R* m) {
+  a0 = CM(m[0], m[1], a0);
+  a1 = CM(m[6], m[7], a1);
+}
+)";
+
+// packed sparse helper: the scalar G_S<z> chain on f32x2 pairs (bit-identical)
+std::string sparse_helper_packed(uint32_t z) {
+  std::ostringstream o;
+  o << "__device__ __forceinline__ void G_S" << z << "(A& a0, A& a1, const R* m) {\n  A b0, b1;\n";
+  for (int r = 0; r < 2; ++r) {
+    const int o0 = 4 * r;
+    // innermost first: m[o0+3] (imag, a1), m[o0+2] (real, a1), m[o0+1] (imag, a0), m[o0] (real, a0)
+    const int ci[4] = {o0 + 3, o0 + 2, o0 + 1, o0 + 0};
+    const char* xv[4] = {"SW(a1)", "a1", "SW(a0)", "a0"};
+    const bool im[4] = {true, false, true, false};
+    std::string acc;
+    for (int i = 0; i < 4; ++i) {
+      if (z >> ci[i] & 1) continue;
+      const std::string coef = std::string(im[i] ? "PI" : "PR") + "(m[" + std::to_string(ci[i]) + "])";
+      acc = acc.empty() ? "fmul2(" + coef + ", " + xv[i] + ")" : "ffma2(" + coef + ", " + xv[i] + ", " + acc + ")";
+    }
+    if (acc.empty()) acc = "qsb::mk<R>(0.f, 0.f)";
+    o << "  " << (r ? "b1" : "b0") << " = " << acc << ";\n";
+  }
+  o << "  a0 = b0; a1 = b1;\n}\n";
+  return o.str();
+}
+
 // A dense 2x2 with statically-zero components dropped from cmac2's FMA chain.  The
 // chain keeps cmac2's association order, and the dropped terms are exact zeros, so
 // the result is bit-identical to the generic kernel's cmac2.
@@ -187,7 +259,17 @@ std::string sparse_helper(uint32_t z) {
 
 // one fused block (qsb_plan.h fuse_phase): a dense 2x2 / 4x4 over register bits qa (matrix
 // bit 0) and qb (bit 1) with its entries at qsb_cf[cf ...]; exact-zero parts dropped
-void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr) {
+// complex64 fused blocks as packed FFMA2 (fma.rn.f32x2): one instruction per complex
+// coefficient part instead of two FFMA -- (mr, mr) * (xr, xi) and (-mi, mi) * (xi, xr), the
+// swapped operand being a free LO_HI operand modifier.  Halves the FP32 instructions of a
+// block (complex64 passes are issue / instruction-fetch bound).  $QSB_JIT_FFMA2=0 disables.
+bool packed_blocks(int c64) {
+  const char* e = getenv("QSB_JIT_FFMA2");
+  if (e && *e) return c64 && atoi(e) == 1;
+  return c64 != 0;
+}
+
+void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr, bool packed) {
   const int d = f.qb < 0 ? 2 : 4;
   const int A = 1 << f.qa, B = f.qb < 0 ? 0 : 1 << f.qb;
   o << "  {  // fused block of " << f.ngates << " gates on register bits " << f.qa;
@@ -199,6 +281,24 @@ void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr) {
     o << "  { const A";
     for (int c = 0; c < d; ++c) o << (c ? ", " : " ") << "x" << c << " = v" << idx[c];
     o << ";\n";
+    if (packed) {
+      for (int r = 0; r < d; ++r) {
+        std::string acc;
+        for (int c = 0; c < d; ++c) {
+          const int e = 2 * (r * d + c);
+          for (int part = 0; part < 2; ++part) {  // 0: real part (mr, mr) * x; 1: (-mi, mi) * swap(x)
+            if (f.m[e + part] == 0.0) continue;
+            const std::string x = part ? "qsb::mk<R>(x" + std::to_string(c) + ".y, x" + std::to_string(c) + ".x)"
+                                       : "x" + std::to_string(c);
+            const std::string k = "qsb_cf2[" + std::to_string(cf + e + part) + "]";
+            acc = "ffma2(" + k + ", " + x + ", " + (acc.empty() ? std::string("qsb::mk<R>(0.f, 0.f)") : acc) + ")";
+          }
+        }
+        o << "    v" << idx[r] << " = " << (acc.empty() ? std::string("qsb::mk<R>(0.f, 0.f)") : acc) << ";\n";
+      }
+      o << "  }\n";
+      continue;
+    }
     for (int r = 0; r < d; ++r) {
       auto chain = [&](bool im) {
         std::string acc;
@@ -255,7 +355,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
   int cf = cf0;
   for (const FuseItem& item : items) {
     if (item.gate < 0) {
-      emit_block(o, item, cf, nr);
+      emit_block(o, item, cf, nr, packed_blocks(c64));
       cf += item.qb < 0 ? 8 : 32;
       continue;
     }
@@ -427,7 +527,18 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   std::ostringstream o;
   for (const char* part : kJitPreludeParts) o << part;
   o << "\ntypedef " << (c64 ? "float" : "double") << " R;\ntypedef " << (c64 ? "float2" : "double2") << " A;\n";
-  o << kHelpers;
+  // packed f32x2 arithmetic pays in the fused complex64 blocks (-6 % DYN20 pass time); the
+  // packed versions of the single-gate helpers (kPackedHelpers, bit-identical) measured no
+  // gain on DYN20 and a loss on RDC30 / VQE24 ($QSB_JIT_PACKED_GATES=1 selects them)
+  const bool packed = packed_blocks(c64);
+  const char* pg = getenv("QSB_JIT_PACKED_GATES");
+  const bool packed_gates = packed && pg && *pg && atoi(pg) == 1;
+  o << (packed_gates ? kPackedHelpers : kHelpers);
+  if (packed && !packed_gates)
+    o << "__device__ __forceinline__ A ffma2(A a, A b, A c) {\n  unsigned long long d;\n"
+         "  asm(\"fma.rn.f32x2 %0, %1, %2, %3;\" : \"=l\"(d) : \"l\"(*reinterpret_cast<unsigned long long*>(&a)), "
+         "\"l\"(*reinterpret_cast<unsigned long long*>(&b)), \"l\"(*reinterpret_cast<unsigned long long*>(&c)));\n"
+         "  return *reinterpret_cast<A*>(&d);\n}\n";
   {  // sparse dense-gate helpers used by this pass
     std::vector<uint32_t> seen;
     for (int g = pd.pgate_begin; g < pd.pgate_begin + pd.pgate_count; ++g) {
@@ -438,7 +549,7 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
       const uint32_t z = zero_mask(ms);
       if (!z || std::find(seen.begin(), seen.end(), z) != seen.end()) continue;
       seen.push_back(z);
-      o << sparse_helper(z);
+      o << (packed_gates ? sparse_helper_packed(z) : sparse_helper(z));
     }
   }
   {  // literal matrices of the pass, indexed by pass-relative gate (exact hex literals)
@@ -453,6 +564,17 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
       }
     }
     if (!pd.pgate_count) o << "0";
+    o << "};\n";
+  }
+  if (!cfv.empty() && packed_blocks(c64)) {  // (mr, mr), (-mi, mi) per complex entry, same indices
+    o << "__constant__ float2 qsb_cf2[" << cfv.size() << "] = {";
+    for (size_t i = 0; i + 1 < cfv.size(); i += 2) {
+      char buf[160];
+      const float mr = (float)cfv[i], mi = (float)cfv[i + 1];
+      snprintf(buf, sizeof(buf), "%s{%af, %af}, {%af, %af}", i ? ", " : "", (double)mr, (double)mr, (double)-mi,
+               (double)mi);
+      o << buf;
+    }
     o << "};\n";
   }
   if (!cfv.empty()) {
