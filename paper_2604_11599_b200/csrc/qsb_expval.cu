@@ -99,20 +99,27 @@ __device__ __forceinline__ double flip_sign(double x, uint32_t zsig, int j) {
   return __hiloint2double(hi, __double2loint(x));
 }
 
+__device__ __forceinline__ float flip_sign(float x, uint32_t zsig, int j) {
+  return __int_as_float(__float_as_int(x) ^ (int)((zsig << (31 - j)) & 0x80000000u));
+}
+
 // sum over the 8 register pairs (j, j ^ XR), j without XR's top bit, of the signed
-// Re / Im part of conj(v_j) v_{j ^ XR}; zsig bit j = Z sign of register j
+// Re / Im part of conj(v_j) v_{j ^ XR}; zsig bit j = Z sign of register j.  The products
+// and the 8-term per-thread sum are in the state's precision (complex64: FP32, well inside
+// the 1e-5 tolerance -- no conversions, half the FP work); everything after (warp, tile and
+// state sums) is FP64.
 template <typename R, int XR>
 __device__ __forceinline__ double ev_pairs(const typename Amp<R>::T* v, uint32_t zsig, bool im) {
   constexpr int TOP = 1 << (31 - __builtin_clz(XR));
-  double acc = 0.0;
+  R acc = (R)0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     if (j & TOP) continue;
-    const double ur = v[j].x, ui = v[j].y, vr = v[j ^ XR].x, vi = v[j ^ XR].y;
-    const double val = im ? fma(ur, vi, -ui * vr) : fma(ur, vr, ui * vi);
+    const R ur = v[j].x, ui = v[j].y, vr = v[j ^ XR].x, vi = v[j ^ XR].y;
+    const R val = im ? fma(ur, vi, -ui * vr) : fma(ur, vr, ui * vi);
     acc += flip_sign(val, zsig, j);
   }
-  return acc;
+  return (double)acc;
 }
 
 // empty asm with the amplitudes as in/out operands: the products of a term are not
@@ -125,10 +132,16 @@ template <typename R>
 __device__ __forceinline__ double ev_term(const typename Amp<R>::T* v, uint32_t xr, uint32_t zsig, bool im) {
   switch (xr) {
     case 0: {
-      double acc = 0.0;
+      if (sizeof(R) == 8) {
+        double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc += flip_sign(norm2<R>(v[j]), zsig, j);
-      return acc;
+        for (int j = 0; j < 16; ++j) acc += flip_sign(norm2<R>(v[j]), zsig, j);
+        return acc;
+      }
+      R acc = (R)0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc += flip_sign(fma(v[j].x, v[j].x, v[j].y * v[j].y), zsig, j);
+      return (double)acc;
     }
 #define QSB_EV_CASE(X) \
   case X: return ev_pairs<R, X>(v, zsig, im);
