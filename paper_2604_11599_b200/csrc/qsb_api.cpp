@@ -74,7 +74,7 @@ struct qsb_ctx_s {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<cudaEvent_t> pass_events;
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
-  int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1;
+  int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1, opt_lowq = 0;
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
   DevBuf shotwords, histo;  // device-side shot histogram (qsb_sample_counts)
   qsb_stats last{};
@@ -120,8 +120,7 @@ int tile_qubits(qsb_ctx ctx, int c64) {
 }
 // contiguous low qubits of every tile: 256-byte runs by default (option low_qubits
 // overrides; shorter runs let a tile cover more qubits of a light cone)
-int64_t g_opt_lowq = 0;
-int low_qubits(int c64) { return g_opt_lowq > 0 ? (int)g_opt_lowq : (c64 ? 5 : 4); }
+int low_qubits(qsb_ctx ctx, int c64) { return ctx->opt_lowq > 0 ? (int)ctx->opt_lowq : (c64 ? 5 : 4); }
 
 // Blocking copy ordered on the context's stream.  ctx->stream is non-blocking, so a plain
 // cudaMemcpy (legacy stream) neither waits for work queued on it nor -- for pageable
@@ -532,7 +531,7 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
-  else if (k == "low_qubits") g_opt_lowq = value;   // 0: default (4 complex128, 5 complex64)      // register-phase gate fusion in the NVRTC kernels    // branch-history deduplication of trajectories
+  else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)      // register-phase gate fusion in the NVRTC kernels    // branch-history deduplication of trajectories
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
     ctx->opt_reg_bits = value;
@@ -1093,7 +1092,7 @@ int sample_traj_impl(qsb_tape tp, int32_t precision, const double* params, uint6
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+    rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(ctx, c64), reg_bits(ctx), &pd);
     if (rc) return rc;
     int64_t B = pick_batch(ctx, t, pd->plan, c64, shot_count);
     QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
@@ -1222,7 +1221,7 @@ int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params,
     finish_stats(ctx, ms, 0, 0, 0, 0, 1, 0, t.n);
   } else {
     PlanDev* pd;
-    rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+    rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(ctx, c64), reg_bits(ctx), &pd);
     if (rc) return rc;
     QSB_CUDA(ctx->state.ensure(amp_bytes(c64) << t.n));
     StreamRun r{tp, pd, c64, 1, ctx->state.p, mats, mstride, seed, shot, d_pre, npredrawn, 0, d_trace, max_trace,
@@ -1283,7 +1282,7 @@ int32_t qsb_apply_tape(qsb_tape tp, const double* params, qsb_state st) {
   rc = prepare_mats(tp, d_params, 1, &mats, &mstride);
   if (rc) return rc;
   PlanDev* pd;
-  rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(ctx, c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   StreamRun r{tp, pd, c64, 1, st->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
   r.in_place = true;
@@ -1339,7 +1338,7 @@ int32_t qsb_statevector(qsb_tape tp, const double* params, qsb_state out) {
     return QSB_OK;
   }
   PlanDev* pd;
-  rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(ctx, c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   StreamRun r{tp, pd, c64, 1, out->amps.p, mats, mstride, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr};
   rc = run_stream(ctx, r);
@@ -1471,7 +1470,7 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
   ctx->run_physical = false;
   RunTimer timer(ctx);
   PlanDev* pd;
-  int rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(c64), reg_bits(ctx), &pd);
+  int rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(ctx, c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   int64_t B = pick_batch(ctx, t, pd->plan, c64, npoints);
   QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
