@@ -328,10 +328,11 @@ void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr, bool p
 // pass time 607.8 -> 594.5 ms per 2048 shots; no callee-saved spills at phase boundaries)
 // for ~1.7x the NVRTC time; complex64 measured 7 % slower inlined.  $QSB_JIT_INLINE_PHASES
 // = 0 / 1 overrides.
-bool inline_phases(int c64) {
+bool inline_phases(int c64, int pass_gates) {
   const char* e = getenv("QSB_JIT_INLINE_PHASES");
   if (e && *e) return atoi(e) == 1;
-  return !c64;
+  const char* mg = getenv("QSB_JIT_INLINE_MIN_GATES");
+  return !c64 && pass_gates >= (mg && *mg ? atoi(mg) : 0);
 }
 
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
@@ -343,7 +344,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
       << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
          "const int tid, A* __restrict__ dst, const uint64_t* __restrict__ hi_off, MID mid) {\n";
   } else {
-    o << (inline_phases(c64) ? "__device__ __forceinline__ void ph" : "__device__ __noinline__ void ph") << ph_index
+    o << (inline_phases(c64, pd.pgate_count) ? "__device__ __forceinline__ void ph" : "__device__ __noinline__ void ph") << ph_index
       << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
          "const int tid) {\n";
   }
@@ -495,15 +496,18 @@ int jit_pass_mode(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
 }
 
 // DIRECT last phase (qsb_pass_common.cuh): complex128 MODE 0 passes without an epilogue
-// whose last phase is a register phase with coalesced stores.  Opt-in ($QSB_LAST_DIRECT=1):
-// measured on B200 it lifts the streaming probe (4.46 -> 4.75 TB/s) but slows VQE24 c128
-// (186 -> 160 points/s); no DYN20 pass qualifies (its last phases hold qubits 0-3 in
-// registers, which would make the stores uncoalesced).
+// and without per-item gate staging whose last phase is a register phase with coalesced
+// stores.  Measured on B200: streaming probe 4.46 -> 4.75 TB/s, RDC30 neutral, no DYN20
+// pass qualifies (its last phases hold qubits 0-3 in registers, which would make the
+// stores uncoalesced); staged passes (ParamRef, VQE24) measured slower, so they are
+// excluded.  $QSB_LAST_DIRECT=0 disables, =2 also allows staged passes.
 bool jit_pass_direct(const TapeInfo& t, const StreamPlan& P, int pass, int c64, int mode) {
   const char* e = getenv("QSB_LAST_DIRECT");
-  if (!(e && *e && atoi(e) == 1)) return false;
+  const int lvl = e && *e ? atoi(e) : 1;
+  if (lvl == 0) return false;
   const PassDesc& pd = P.passes[pass];
   if (c64 || mode != 0 || pd.epi || pd.phase_count < 1) return false;
+  if (lvl < 2 && pass_needs_stage(t, P, pass)) return false;
   const PhaseDesc& ph = P.phases[pd.phase_begin + pd.phase_count - 1];
   if (ph.nt < 3) return false;
   // coalesced stores: lanes 0..7 of a warp must cover 8 consecutive amplitudes (128 B)
