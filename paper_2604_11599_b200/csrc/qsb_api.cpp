@@ -192,10 +192,16 @@ int get_plan(qsb_tape tp, int c64, int k, int lowq, int rb, PlanDev** out) {
     for (size_t i = 0; i < P.passes.size(); ++i)
       if (P.passes[i].phase_count && pd->jit[i].kern) pd->pflops[i] = pass_flops_fused(tp->info, P, (int)i);
   if (getenv("QSB_PLAN_DEBUG"))
-    for (size_t i = 0; i < P.passes.size(); ++i)
-      fprintf(stderr, "pass %zu: k %d gates %d phases %d flops/state %.4g (unfused %.4g) epi %d\n", i, P.passes[i].k,
-              P.passes[i].pgate_count, P.passes[i].phase_count, pd->pflops[i], pass_flops(tp->info, P, (int)i),
-              P.passes[i].epi);
+    for (size_t i = 0; i < P.passes.size(); ++i) {
+      fprintf(stderr, "pass %zu: k %d gates %d phases %d flops/state %.4g (unfused %.4g) epi %d last-phase tpos", i,
+              P.passes[i].k, P.passes[i].pgate_count, P.passes[i].phase_count, pd->pflops[i],
+              pass_flops(tp->info, P, (int)i), P.passes[i].epi);
+      if (P.passes[i].phase_count) {
+        const PhaseDesc& ph = P.phases[P.passes[i].phase_begin + P.passes[i].phase_count - 1];
+        for (int b = 0; b < ph.nt && b < 16; ++b) fprintf(stderr, " %d", ph.tpos[b]);
+      }
+      fprintf(stderr, "\n");
+    }
   *out = pd.get();
   tp->plans[key] = std::move(pd);
   return QSB_OK;

@@ -510,9 +510,19 @@ bool jit_pass_direct(const TapeInfo& t, const StreamPlan& P, int pass, int c64, 
   if (lvl < 2 && pass_needs_stage(t, P, pass)) return false;
   const PhaseDesc& ph = P.phases[pd.phase_begin + pd.phase_count - 1];
   if (ph.nt < 3) return false;
-  // coalesced stores: lanes 0..7 of a warp must cover 8 consecutive amplitudes (128 B)
-  for (int i = 0; i < 3; ++i)
-    if (ph.tpos[i] != i) return false;
+  // store coalescing: with s of the tile positions 0..s-1 in registers (each thread owns
+  // 2^s consecutive amplitudes), lanes advance by 2^s amplitudes and a warp store covers
+  // 16-byte pieces of 2^s * 16-byte runs that the thread's other registers complete
+  // (merged in L2).  s <= $QSB_LAST_DIRECT_MAXLOW (default 0: lanes 0..7 cover 128 B).
+  const char* ml = getenv("QSB_LAST_DIRECT_MAXLOW");
+  const int maxlow = ml && *ml ? atoi(ml) : 0;
+  uint32_t tmask = 0;
+  for (int i = 0; i < ph.nt; ++i) tmask |= 1u << ph.tpos[i];
+  int s = 0;
+  while (s < pd.k && !(tmask >> s & 1)) ++s;  // low positions held in registers
+  if (s > maxlow) return false;
+  for (int i = 0; i < 3; ++i)  // the next three tile positions are the lanes' low bits
+    if (ph.tpos[i] != s + i) return false;
   return true;
 }
 
