@@ -323,6 +323,11 @@ void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr, bool p
   o << "  }\n";
 }
 
+bool edge_x_disabled() {
+  const char* e = getenv("QSB_JIT_EDGE_X");
+  return e && *e && atoi(e) == 0;
+}
+
 // Phases are separate __noinline__ functions (ptxas time linear in the phases) except for
 // complex128, where inlining them into the pass kernel measured 2.2 % faster on B200 (DYN20
 // pass time 607.8 -> 594.5 ms per 2048 shots; no callee-saved spills at phase boundaries)
@@ -351,10 +356,52 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
   o << "  const uint32_t base = 0u";
   for (int i = 0; i < ph.nt; ++i) o << " | ((((uint32_t)tid >> " << i << ") & 1u) << " << (int)ph.tpos[i] << ")";
   o << ";\n  const uint32_t sb = base ^ swz[base >> " << sb << "];\n";
-  for (int j = 0; j < nr; ++j) o << "  A v" << j << " = tile[sb ^ " << ph.soff[j] << "u];\n";
+  // X gates with a per-item condition (control outside the tile, or an if-guard) that
+  // commute to the start or the end of the phase become a conditional XOR of the thread's
+  // slot base at the phase's loads / stores (the slot map is XOR-linear in the register
+  // index) instead of a branch whose join needs 2 x 16 register moves
+  std::vector<int> edge(items.size(), 0);  // 1: at the loads, 2: at the stores
+  if (!edge_x_disabled()) {
+    auto bits_of = [&](const FuseItem& it) -> uint32_t {
+      if (it.gate < 0) return (1u << it.qa) | (it.qb >= 0 ? 1u << it.qb : 0u);
+      const PhaseGate& q = P.phase_gates[it.gate];
+      switch (q.kind) {
+        case PK_DENSE: case PK_XPERM: case PK_ANTI: case PK_DIAG_R: return q.cmR | (1u << q.jt);
+        case PK_DIAG_T: case PK_DIAG_G: return q.cmR;
+        default: return ~0u;
+      }
+    };
+    for (size_t i = 0; i < items.size(); ++i) {
+      if (items[i].gate < 0) continue;
+      const PhaseGate& q = P.phase_gates[items[i].gate];
+      if (q.kind != PK_XPERM || q.cmR || q.cmT || !(q.guard >= 0 || q.gcm != 0)) continue;
+      bool front = true, back = !direct;
+      for (size_t j = 0; j < items.size(); ++j) {
+        if (j == i || edge[j] == 1) continue;  // earlier front-moved X gates commute with it
+        if (!(bits_of(items[j]) >> q.jt & 1)) continue;
+        if (j < i) front = false;
+        else back = false;
+      }
+      if (front) edge[i] = 1;
+      else if (back) edge[i] = 2;
+    }
+  }
+  auto edge_flip = [&](int which, const char* name) {
+    o << "  uint32_t " << name << " = 0u;\n";
+    for (size_t i = 0; i < items.size(); ++i)
+      if (edge[i] == which) {
+        const PhaseGate& q = P.phase_gates[items[i].gate];
+        o << "  if (sg[" << (items[i].gate - pd.pgate_begin) << "].kind != " << (int)PK_SKIP << ") " << name
+          << " ^= " << ph.soff[1 << q.jt] << "u;\n";
+      }
+  };
+  edge_flip(1, "fl_in");
+  for (int j = 0; j < nr; ++j) o << "  A v" << j << " = tile[(sb ^ fl_in) ^ " << ph.soff[j] << "u];\n";
   if (direct) o << "  mid();\n";
   int cf = cf0;
-  for (const FuseItem& item : items) {
+  for (size_t ii = 0; ii < items.size(); ++ii) {
+    const FuseItem& item = items[ii];
+    if (edge[ii]) continue;
     if (item.gate < 0) {
       emit_block(o, item, cf, nr, packed_blocks(c64));
       cf += item.qb < 0 ? 8 : 32;
@@ -462,7 +509,8 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
       o << "  dst[tof | " << off << "ull] = v" << j << ";\n";
     }
   } else {
-    for (int j = 0; j < nr; ++j) o << "  tile[sb ^ " << ph.soff[j] << "u] = v" << j << ";\n";
+    edge_flip(2, "fl_out");
+    for (int j = 0; j < nr; ++j) o << "  tile[(sb ^ fl_out) ^ " << ph.soff[j] << "u] = v" << j << ";\n";
   }
   o << "}\n";
 }
