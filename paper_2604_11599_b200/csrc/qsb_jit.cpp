@@ -374,7 +374,9 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
     for (size_t i = 0; i < items.size(); ++i) {
       if (items[i].gate < 0) continue;
       const PhaseGate& q = P.phase_gates[items[i].gate];
-      if (q.kind != PK_XPERM || q.cmR || q.cmT || !(q.guard >= 0 || q.gcm != 0)) continue;
+      // per-item (guard / out-of-tile control) or per-thread (control on a thread
+      // position) condition; an unconditional X is a free register renaming anyway
+      if (q.kind != PK_XPERM || q.cmR || !(q.guard >= 0 || q.gcm != 0 || q.cmT != 0)) continue;
       bool front = true, back = !direct;
       for (size_t j = 0; j < items.size(); ++j) {
         if (j == i || edge[j] == 1) continue;  // earlier front-moved X gates commute with it
@@ -391,8 +393,13 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
     for (size_t i = 0; i < items.size(); ++i)
       if (edge[i] == which) {
         const PhaseGate& q = P.phase_gates[items[i].gate];
-        o << "  if (sg[" << (items[i].gate - pd.pgate_begin) << "].kind != " << (int)PK_SKIP << ") " << name
-          << " ^= " << ph.soff[1 << q.jt] << "u;\n";
+        std::string cond;
+        if (q.guard >= 0 || q.gcm != 0)
+          cond = "sg[" + std::to_string(items[i].gate - pd.pgate_begin) + "].kind != " + std::to_string((int)PK_SKIP);
+        if (q.cmT)
+          cond += std::string(cond.empty() ? "" : " && ") + "(base & " + std::to_string(q.cmT) + "u) == " +
+                  std::to_string(q.cvT) + "u";
+        o << "  if (" << cond << ") " << name << " ^= " << ph.soff[1 << q.jt] << "u;\n";
       }
   };
   edge_flip(1, "fl_in");
