@@ -476,3 +476,28 @@ def test_fusion_random_local_circuits(prec, seed):
             flops[fuse] = st["pass_flops"]
             assert_state(got, want, TOL[prec])
     assert flops[1] < flops[0], flops
+
+
+@pytest.mark.gpu
+def test_rdc30_full_size_properties():
+    """BASELINE cfg 4 at full size (30 qubits, two measurement rounds): size-independent
+    properties where the oracle cannot follow -- the final state stays normalised (1e-10
+    complex128 / 1e-5 complex64), the measured register is identical in both precisions
+    (no decision inside the tie band), and a static 28-qubit circuit followed by its exact
+    inverse returns |0...0> (every <Z_k> = 1 within 1e-10)."""
+    _, k = workloads.rdc_circuit(n=30, depth=40, every=20, seed=30200)
+    b = ir.bind(k, [])
+    keys = {}
+    for prec, tol in (("c128", 1e-10), ("c64", 1e-5)):
+        store, st = sim.run_trajectory(b, sim.RngStream.for_shot(1234, 0), precision=prec)
+        assert abs(st.norm() - 1.0) <= tol, (prec, st.norm())
+        keys[prec] = store.key()
+        del st
+    assert keys["c128"] == keys["c64"], keys
+    fwd = [op for op in workloads.rdc_circuit(n=28, depth=12, every=100, seed=7)[1].body if isinstance(op, ir.Gate)]
+    inv = [ir.Gate(g.base, g.angles, g.targets, g.controls, not g.adjoint) for g in reversed(fwd)]
+    st = sim.statevector(ir.bind(ir.Kernel(28, [("q", 28)], [], [], fwd + inv), []))
+    assert abs(st.norm() - 1.0) <= 1e-10
+    for q in range(28):
+        z = sim.expval_pauli(st, "".join("Z" if i == q else "I" for i in range(28)))
+        assert z >= 1.0 - 1e-10, (q, z)
