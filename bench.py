@@ -278,7 +278,7 @@ def run_ours(args) -> None:
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "qubits": 20, "batch_per_gpu": B, "shots_per_step": B * world,
                        "precision": "complex128" if prec == "c128" else "complex64", "seed": SEED,
-                       "l2": f"inputs larger than L2: {B} x 16 MiB states per GPU",
+                       "l2": f"inputs larger than L2: {B} x {16 if prec == 'c128' else 8} MiB states per GPU",
                        "engine": "streaming (fused passes + decide)", "tile_qubits": ctx.stats()["tile_qubits"]},
             "gate_updates_per_s": gate_updates_all / (dev_ms_max / 1000.0),
             "tie_band_decisions": int(ties_all),
@@ -317,7 +317,8 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=4096, help="trajectories per GPU per step")
+    ap.add_argument("--batch", type=int, default=8192,
+                    help="trajectories per GPU per step (8192 x 16 MiB = 128 GiB of complex128 states)")
     ap.add_argument("--precision", choices=["c128", "c64"], default="c128")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
