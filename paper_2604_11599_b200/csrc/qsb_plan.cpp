@@ -245,6 +245,7 @@ struct Planner {
   int swz_bits_ = 3;
   bool pair_aware_ = getenv("QSB_PAIR_AWARE") ? atoi(getenv("QSB_PAIR_AWARE")) != 0 : true;
   bool phase_search_ = getenv("QSB_PHASE_SEARCH") ? atoi(getenv("QSB_PHASE_SEARCH")) != 0 : false;
+  bool block_condx_ = getenv("QSB_BLOCK_CONDX") ? atoi(getenv("QSB_BLOCK_CONDX")) != 0 : false;
   StreamPlan& P;
   std::vector<RegionBuild> regions;
 
@@ -366,16 +367,25 @@ struct Planner {
             break;
           }
         }
+        bool took = false;
         if (want && popc(R | want) <= rb) {
           R |= want;
           take.push_back(gi);
+          took = true;
         } else if (popc(R | need) <= rb) {
           R |= need;
           take.push_back(gi);
+          took = true;
         } else {
           rest.push_back(gi);
           blocked |= touched;
         }
+        // an X whose condition is per item (out-of-tile control, guard) or per thread
+        // (control on a thread position) ends its target's use in this phase, so that the
+        // code generator can fold it into the phase's store addresses (edge X) instead of
+        // a branch or per-pair selects
+        if (took && block_condx_ && g.gclass == GC_XPERM && ((g.lcm & ~R) || g.gcm || g.guard >= 0))
+          blocked |= 1u << g.lt;
       }
       for (int p = 0; p < k && popc(R) < rb; ++p) R |= 1u << p;
       PhaseDesc ph{};
