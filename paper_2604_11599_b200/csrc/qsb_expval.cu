@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "qsb_device.cuh"
 #include "qsb_launch.h"
@@ -32,6 +33,13 @@ namespace qsb {
 namespace {
 
 constexpr int kET = 256;
+#ifndef QSB_EV_L2_PREFETCH
+#define QSB_EV_L2_PREFETCH 0
+#endif
+// L2 prefetch of the next item's runs in the register-mapped reducer: measured on B200 to
+// make run-to-run times unstable (complex64 VQE24 reducer 53 - 130 ms per 32 points across
+// processes) for no gain in the good case; off
+constexpr bool kEvL2Prefetch = QSB_EV_L2_PREFETCH != 0;
 
 __device__ __forceinline__ void prefetch_line_l2(const void* gmem) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(gmem));
@@ -160,8 +168,8 @@ __global__ void __launch_bounds__(kET, 2) k_expval_reg(const typename Amp<R>::T*
                                                       const EvMap* __restrict__ maps, double* __restrict__ partial,
                                                       int nterm_total) {
   // persistent: the per-CTA tables are built once, then the CTA walks (slot, tile)
-  // items with a grid stride, prefetching the next item's runs into L2 while the
-  // current one is evaluated
+  // items with a grid stride (the L2 prefetch of the next item's runs is compiled out:
+  // kEvL2Prefetch)
   using A = typename Amp<R>::T;
   constexpr int SB = sizeof(R) == 8 ? 3 : 4;
   constexpr int K = 12, TL = 1 << K, NT = K - 4;
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(kET, 2) k_expval_reg(const typename Amp<R>::T*
     const int64_t slot = w >> ntl;
     const uint64_t base = pdep64((uint64_t)(w & (tiles - 1)), outmask);
     const A* st = states + (slot << n);
-    {  // next item's runs into L2
+    if (kEvL2Prefetch) {  // next item's runs into L2
       const int64_t wn = w + gridDim.x;
       if (wn < W) {
         const A* sn = states + ((wn >> ntl) << n) + pdep64((uint64_t)(wn & (tiles - 1)), outmask);
@@ -308,23 +316,40 @@ void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const
                         sizeof(uint32_t) * ((size_t)1 << (g.k - (c64 ? 4 : 3))) +
                         sizeof(double) * (kET / 32) * (size_t)g.nterm + sizeof(ExpvalTerm) * (size_t)g.nterm +
                         sizeof(EvMap) * (size_t)g.nmap + 16 + sizeof(double) * 8 * kET;
-    int dev = 0, sms = 148, per_sm = 1;
+    // driver queries cached per (device, precision, smem): a group launch stays a pure
+    // enqueue (no attribute / occupancy calls between the kernels of an observe)
+    struct OccKey { int dev, c64; size_t smem; };
+    static thread_local std::vector<std::pair<OccKey, int>> occ;  // -> resident CTAs on the device
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int resident = 0;
+    for (const auto& e : occ)
+      if (e.first.dev == dev && e.first.c64 == c64 && e.first.smem == smem) resident = e.second;
+    if (!resident) {
+      // the attribute is a ceiling: set it to the device's opt-in maximum once, so that
+      // cached launches of any group size stay valid
+      int sms = 148, per_sm = 1, optin = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      const int cap = std::max(optin, (int)smem);
+      if (c64) {
+        cudaFuncSetAttribute(k_expval_reg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expval_reg<float>, kET, smem);
+      } else {
+        cudaFuncSetAttribute(k_expval_reg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expval_reg<double>, kET, smem);
+      }
+      resident = std::max(1, per_sm) * sms;
+      occ.push_back({OccKey{dev, c64, smem}, resident});
+    }
     const int64_t W = (int64_t)grid.x * slots;
-    if (c64) {
-      cudaFuncSetAttribute(k_expval_reg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expval_reg<float>, kET, smem);
-      const unsigned pg = (unsigned)std::min<int64_t>(W, (int64_t)std::max(1, per_sm) * sms);
+    const unsigned pg = (unsigned)std::min<int64_t>(W, (int64_t)resident);
+    if (c64)
       k_expval_reg<float><<<pg, kET, smem, s>>>((const float2*)states, n, slots, g, terms, maps, partial,
                                                 nterm_total);
-    } else {
-      cudaFuncSetAttribute(k_expval_reg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expval_reg<double>, kET, smem);
-      const unsigned pg = (unsigned)std::min<int64_t>(W, (int64_t)std::max(1, per_sm) * sms);
+    else
       k_expval_reg<double><<<pg, kET, smem, s>>>((const double2*)states, n, slots, g, terms, maps, partial,
                                                  nterm_total);
-    }
     return;
   }
   const size_t smem = amp * ((size_t)1 << g.k) + sizeof(uint64_t) * ((size_t)1 << (g.k - g.lowq)) +
