@@ -185,6 +185,7 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2604_11599_b200 import _lib, ir, sim, workloads
+    from paper_2604_11599_b200 import dist as qdist
 
     ctx = _lib.context(local)
     _, kernel = workloads.dyn_circuit()
@@ -232,7 +233,10 @@ def run_ours(args) -> None:
     e2e_steps = max(1, min(args.steps, 3))
     hists = []
     for s in range(e2e_steps):
-        hists.append(sim.sample(bound, B, SEED, precision=prec, device=local))
+        if world > 1:  # one job of B x world shots, contiguous shot ranges per rank, merged histogram
+            hists.append(qdist.sample_sharded(bound, B * world, SEED, precision=prec, device=local))
+        else:
+            hists.append(sim.sample(bound, B, SEED, precision=prec, device=local))
     torch.cuda.synchronize(local)
     e2e_s = time.perf_counter() - t0
     # sim.sample histograms on the device: per-shot status words + the distinct outcomes
@@ -299,7 +303,8 @@ def run_ours(args) -> None:
                                  "flops_per_step": flops / args.steps},
             "jit_passes": jit_passes,
             "e2e": {"value": e2e_value, "unit": "shots/s", "h2d_bytes_per_step": h2d_bytes,
-                    "d2h_bytes_per_step": d2h_bytes, "api": "paper_2604_11599_b200.sim.sample"},
+                    "d2h_bytes_per_step": d2h_bytes, "api": "paper_2604_11599_b200.sim.sample" if world == 1
+                    else "paper_2604_11599_b200.dist.sample_sharded"},
             "gpu_launches": int(launches_all),
             "clocks": clocks.summary(),
         }

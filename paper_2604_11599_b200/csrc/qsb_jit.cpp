@@ -767,6 +767,10 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
     }
     int per_sm = 1, dev = 0, sms = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, jk.threads, jk.smem);
+    // $QSB_JIT_CTAS_PER_SM caps the persistent grid (experiment: two contexts on two
+    // streams sharing the SMs, experiments/two_stream.py)
+    if (const char* e = getenv("QSB_JIT_CTAS_PER_SM"))
+      if (atoi(e) > 0) per_sm = std::min(per_sm, atoi(e));
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     jk.max_grid = (int64_t)std::max(1, per_sm) * sms;
