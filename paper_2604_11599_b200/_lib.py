@@ -130,7 +130,7 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("QSB_LIB") or LIB_PATH  # QSB_LIB: A/B builds (experiments)
         if not os.path.exists(p):
             _lib_error = f"{p} not built (run `python -c 'import __graft_entry__ as g; g.build()'`)"
             raise NativeLibraryMissing(_lib_error)
