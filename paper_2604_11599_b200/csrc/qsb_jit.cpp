@@ -48,6 +48,7 @@ struct Nvrtc {
   decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
   decltype(&nvrtcGetProgramLog) log = nullptr;
   decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  int major = 0, minor = 0;  // nvrtcVersion (part of the cubin cache key)
   bool ok = false;
 };
 
@@ -55,11 +56,21 @@ Nvrtc& nvrtc() {
   static Nvrtc n;
   static std::once_flag once;
   std::call_once(once, [] {
-    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so"}) {
+    // the toolkit's NVRTC first, by path: a process that imported torch already has the
+    // wheel's libnvrtc.so.12 (12.8) mapped, which a soname lookup would return, and its
+    // ptxas materialises the swapped FFMA2 operands of the complex64 blocks as MOV pairs
+    // (measured on B200: 20 % of a DYN20 c64 pass's instructions) where 12.9 uses the
+    // free LO_HI operand swizzle.  $QSB_NVRTC overrides.
+    const char* env = getenv("QSB_NVRTC");
+    for (const char* name : {env && *env ? env : "", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
+                             "libnvrtc.so"}) {
+      if (!*name) continue;
       n.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
       if (n.h) break;
     }
     if (!n.h) return;
+    auto ver = (nvrtcResult(*)(int*, int*))dlsym(n.h, "nvrtcVersion");
+    if (ver) ver(&n.major, &n.minor);
     n.create = (decltype(n.create))dlsym(n.h, "nvrtcCreateProgram");
     n.compile = (decltype(n.compile))dlsym(n.h, "nvrtcCompileProgram");
     n.cubin_size = (decltype(n.cubin_size))dlsym(n.h, "nvrtcGetCUBINSize");
@@ -707,6 +718,7 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
     j.src = jit_source(t, P, i, c64, fuse);
     std::string key = j.src;
     for (const char* opt : kOpts) key += opt;
+    key += "nvrtc " + std::to_string(nvrtc().major) + "." + std::to_string(nvrtc().minor);
     char name[64];
     snprintf(name, sizeof(name), "/%016llx.cubin", (unsigned long long)fnv1a(key));
     j.path = dir + name;
