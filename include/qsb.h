@@ -224,6 +224,11 @@ int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqubits, int32
 int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
                          int32_t precision, int32_t reg_bits, double* out);
 
+/* host-only: version of the NVRTC library the pass generator compiles with (opened on first
+ * use: $QSB_NVRTC, then the toolkit's /usr/local/cuda/lib64/libnvrtc.so.12, then the
+ * soname).  QSB_ERR_ARG when no NVRTC can be loaded.                                   */
+int32_t qsb_jit_nvrtc_version(int32_t* major, int32_t* minor);
+
 /* host-only: register-phase gate fusion of the NVRTC kernels (qsb_plan.h fuse_phase) over
  * a tape's streaming plan (tile 12).  out[0..5] = {phases, fused blocks, gates folded into
  * blocks, host-check failures, pass flops per state unfused, the same fused}.          */

@@ -110,6 +110,7 @@ _SIGS = {
     "qsb_debug_rng": (_I32, [_P, _U64, _I64, _I32, _P]),
     "qsb_plan_summary": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "qsb_jit_selftest": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "qsb_jit_nvrtc_version": (_I32, [_P, _P]),
     "qsb_fusion_stats": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "qsb_debug_fma_peak": (_I32, [_P, _I32, _PD]),
     "qsb_state_prob1": (_I32, [_P, _I32, _PD]),

@@ -1596,6 +1596,16 @@ extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqu
   return QSB_OK;
 }
 
+extern "C" int32_t qsb_jit_nvrtc_version(int32_t* major, int32_t* minor) {
+  if (!major || !minor) return fail(QSB_ERR_ARG, "null output");
+  int a = 0, b = 0;
+  jit_nvrtc_version(&a, &b);
+  *major = a;
+  *minor = b;
+  if (!jit_available()) return fail(QSB_ERR_ARG, "libnvrtc not loadable");
+  return QSB_OK;
+}
+
 extern "C" int32_t qsb_fusion_stats(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits,
                                     int32_t nparams, int32_t precision, int32_t reg_bits, double* out) {
   const int c64 = precision == QSB_C64 ? 1 : 0;

@@ -537,6 +537,11 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
 
 bool jit_available() { return nvrtc().ok; }
 
+void jit_nvrtc_version(int* major, int* minor) {
+  *major = nvrtc().major;
+  *minor = nvrtc().minor;
+}
+
 // staging is needed only if a phase reads the staged gates: per-item skips (guards,
 // out-of-tile controls, per-tile diagonal factors), non-literal matrices, swap phases
 bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass) {

@@ -20,6 +20,8 @@ struct JitKernel {
 
 // true if libnvrtc could be loaded
 bool jit_available();
+// the loaded NVRTC's version (0.0 when none)
+void jit_nvrtc_version(int* major, int* minor);
 
 // true if a phase of the pass reads the per-item staged gates (see pass_persistent)
 bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass);

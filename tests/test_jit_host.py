@@ -71,3 +71,23 @@ def test_phase_fusion_host_check(precision, reg_bits):
     k3 = workloads.random_static(14, 300, seed=9, nparams=2, max_controls=2)
     st3 = _fusion_stats(k3, precision, reg_bits)
     assert st3[3] == 0 and st3[5] <= st3[4], st3
+
+
+def test_nvrtc_is_the_toolkit_library_even_after_torch():
+    """The pass generator compiles with the toolkit's NVRTC, not the older copy a torch
+    import maps under the same soname (whose ptxas turned the complex64 blocks' swapped
+    FFMA2 operands into MOV pairs: DYN20 c64 4170 vs 4617 shots/s on B200)."""
+    import os
+
+    import torch  # noqa: F401  (maps the wheel's libnvrtc.so.12 first, as bench.py does)
+
+    path = "/usr/local/cuda/lib64/libnvrtc.so.12"
+    if not os.path.exists(path):
+        pytest.skip("no toolkit NVRTC here")
+    tk = ctypes.CDLL(path)
+    a, b = ctypes.c_int(), ctypes.c_int()
+    tk.nvrtcVersion(ctypes.byref(a), ctypes.byref(b))
+    lib = _lib.load()
+    ma, mi = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(lib.qsb_jit_nvrtc_version(ctypes.byref(ma), ctypes.byref(mi)))
+    assert (ma.value, mi.value) == (a.value, b.value)
