@@ -14,9 +14,15 @@ e2e    : the same shots through the public API `sim.sample(bound, B, seed)`
          (host wall clock, includes parameter upload, key download, histogram).
 roofline: the fused pass kernel (k_pass): algorithmic bytes 2 * 2^n * 16 B per state
          per pass (1x for the first, write-only pass) / its CUDA-event time.
---impl reference: the CPU oracle port (oracle/sim_port.py, a numpy restatement of the
-         reference simulator, pinned bit-exact to it) on the host cores, one process
-         per core, a bounded sample of DYN20 shots per step.
+--impl reference: the UNMODIFIED reference simulator installed in baseline/_ref
+         (`pip install --target baseline/_ref`) through its public API
+         (`qasm2cudaq.suites.compile_source` -> `kir.bind` -> `sim.run_trajectory` with
+         `RngStream.for_shot`, the unit of work of `sim.sample`'s process pool,
+         sim.py:346-391) on all host cores, one shot per process per step; the pinned
+         oracle port (oracle/sim_port.py) only when baseline/_ref is absent.
+--gpus N: without a launcher-provided WORLD_SIZE, bench.py re-launches itself under
+         `torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL); it exits
+         non-zero when fewer than N GPUs are visible.
 """
 
 from __future__ import annotations
@@ -111,24 +117,79 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def _cpu_shot(args):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    sys.path.insert(0, REPO)
-    from oracle import sim_port as P
-    from paper_2604_11599_b200 import ir, workloads
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
 
-    shot, n, layers = args
-    _, k = workloads.dyn_circuit(n=n, layers=layers)
-    b = ir.bind(k, [])
+
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "qasm2cudaq"))
+
+
+def host_info() -> dict:
+    """nproc / CPU model / RAM of the host the CPU arm ran on."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    info["ram_gib"] = round(int(line.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keep = ("Socket(s)", "Core(s) per socket", "Thread(s) per core", "NUMA node(s)")
+        info["lscpu"] = {k.strip(): v.strip() for k, _, v in (ln.partition(":") for ln in out.splitlines())
+                         if k.strip() in keep}
+    except Exception:
+        pass
+    return info
+
+
+_REF_BOUND = {}
+
+
+def _ref_shot(args):
+    """One DYN20 shot through the UNMODIFIED reference (baseline/_ref)."""
+    shot, kind = args
+    if not _REF_BOUND:
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        sys.path.insert(0, REPO)
+        from paper_2604_11599_b200 import workloads
+
+        src, k = workloads.dyn_circuit()
+        if kind == "reference":
+            sys.path.insert(0, REF_DIR)
+            from qasm2cudaq import kir, sim, suites
+
+            _REF_BOUND["run"] = lambda s: sim.run_trajectory(kir.bind(_REF_BOUND["k"], []),
+                                                             sim.RngStream.for_shot(SEED, s))[0].key()
+            _REF_BOUND["k"] = suites.compile_source(src)
+        else:
+            from oracle import sim_port as P
+            from paper_2604_11599_b200 import ir
+
+            b = ir.bind(k, [])
+            _REF_BOUND["run"] = lambda s: P.trajectory(b, P.PortRng.for_shot(SEED, s))[0].key()
     t0 = time.perf_counter()
-    store, _ = P.trajectory(b, P.PortRng.for_shot(SEED, shot))
-    return store.key(), time.perf_counter() - t0
+    key = _REF_BOUND["run"](shot)
+    return key, time.perf_counter() - t0
 
 
 def cpu_baseline(steps: int, warmup: int, shots_per_step: int | None = None) -> dict:
-    """Oracle port on all host cores (process pool, 1 BLAS thread each)."""
+    """The reference CPU path on all host cores: a process pool (1 BLAS thread per
+    process, the reference's own recipe for linear scaling), one
+    DYN20 shot per process per step, global shots continuing across steps."""
     import multiprocessing as mp
 
+    kind = "reference" if reference_available() else "port"
     cores = os.cpu_count() or 1
     per = shots_per_step or cores
     ctx = mp.get_context("spawn")
@@ -139,7 +200,7 @@ def cpu_baseline(steps: int, warmup: int, shots_per_step: int | None = None) -> 
     with ctx.Pool(processes=min(cores, per)) as pool:
         for step in range(warmup + steps):
             t0 = time.perf_counter()
-            pool.map(_cpu_shot, [(shot + i, 20, 40) for i in range(per)])
+            pool.map(_ref_shot, [(shot + i, kind) for i in range(per)], chunksize=1)
             dt = time.perf_counter() - t0
             shot += per
             if step >= warmup:
@@ -147,10 +208,20 @@ def cpu_baseline(steps: int, warmup: int, shots_per_step: int | None = None) -> 
     if env_before is None:
         os.environ.pop("OPENBLAS_NUM_THREADS", None)
     total = sum(times)
-    return {"value": per * len(times) / total, "unit": "shots/s", "cores": min(cores, per), "kind": "port",
-            "sample": f"{per * len(times)} DYN20 shots ({per} per step, one per process, numpy oracle port "
-                      f"oracle/sim_port.py, OPENBLAS_NUM_THREADS=1), {total:.1f} s",
-            "ms_per_step": 1000 * total / len(times)}
+    what = ("the unmodified reference qasm2cudaq (baseline/_ref) sim.run_trajectory" if kind == "reference"
+            else "the numpy oracle port oracle/sim_port.py")
+    return {"value": per * len(times) / total, "unit": "shots/s", "cores": min(cores, per), "kind": kind,
+            "sample": f"{per * len(times)} DYN20 shots ({per} per step, one per process, {what}, "
+                      f"OPENBLAS_NUM_THREADS=1), {total:.1f} s",
+            "host": host_info(), "ms_per_step": 1000 * total / len(times)}
+
+
+def base_config(batch: int, world: int, prec: str) -> dict:
+    """The workload description shared by both arms (same keys, so the driver's
+    same-config check compares like with like)."""
+    return {"workload": WORKLOAD, "qubits": 20, "batch_per_gpu": batch, "shots_per_step": batch * world,
+            "precision": "complex128" if prec == "c128" else "complex64", "seed": SEED,
+            "l2": f"inputs larger than L2: {batch} x {16 if prec == 'c128' else 8} MiB states per GPU"}
 
 
 def run_reference(args) -> None:
@@ -158,11 +229,14 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     cb = cpu_baseline(args.steps, args.warmup)
+    cfg = base_config(args.batch, args.gpus, args.precision)
+    cfg["engine"] = "CPU: " + ("reference qasm2cudaq sim (baseline/_ref)" if cb["kind"] == "reference"
+                               else "oracle port of the reference sim")
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "shots/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "qubits": 20, "seed": SEED},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": cfg,
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
             "e2e": {"value": cb["value"], "unit": "shots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -180,9 +254,18 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < (local + 1):
+        sys.exit(f"bench.py: rank {rank} needs GPU {local}, {torch.cuda.device_count()} visible")
+    comm = {"backend": None, "world_size": world}
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version()),
+                "data_path_collectives": 0,
+                "collectives": "barrier + all_reduce(MAX) of the device times + all_gather of the e2e histogram"}
 
     from paper_2604_11599_b200 import _lib, ir, sim, workloads
     from paper_2604_11599_b200 import dist as qdist
@@ -196,7 +279,7 @@ def run_ours(args) -> None:
     h2d_bytes = 8  # the step's seed / shot offset; DYN20 has no parameters
 
     def step_shots(step):  # disjoint global shot ranges per (step, rank)
-        return (step * world + rank) * B
+        return step_shot_begin(step, rank, world, B)
 
     def barrier():
         if world > 1:
@@ -243,13 +326,8 @@ def run_ours(args) -> None:
     # (8-byte word + 4-byte count each) + the distinct count come back
     d2h_bytes = B * 4 + 4 + 12 * len(hists[-1].counts)
 
-    t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-    g = torch.tensor([gate_updates, ties, launches], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(g, op=dist.ReduceOp.SUM)
-    dev_ms_max, e2e_max = t.tolist()
-    gate_updates_all, ties_all, launches_all = g.tolist()
+    (dev_ms_max, e2e_max), (gate_updates_all, ties_all, launches_all) = reduce_over_ranks(
+        [dev_ms, e2e_s], [gate_updates, ties, launches], f"cuda:{local}")
     shots_total = B * args.steps * world
     value = shots_total / (dev_ms_max / 1000.0)
     e2e_value = B * e2e_steps * world / e2e_max
@@ -280,10 +358,9 @@ def run_ours(args) -> None:
             "vs_baseline": None,
             "dtype": "f64" if prec == "c128" else "f32",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "qubits": 20, "batch_per_gpu": B, "shots_per_step": B * world,
-                       "precision": "complex128" if prec == "c128" else "complex64", "seed": SEED,
-                       "l2": f"inputs larger than L2: {B} x {16 if prec == 'c128' else 8} MiB states per GPU",
-                       "engine": "streaming (fused passes + decide)", "tile_qubits": ctx.stats()["tile_qubits"]},
+            "config": {**base_config(B, world, prec), "engine": "streaming (fused passes + decide)"},
+            "tile_qubits": ctx.stats()["tile_qubits"],
+            "comm": comm,
             "gate_updates_per_s": gate_updates_all / (dev_ms_max / 1000.0),
             "tie_band_decisions": int(ties_all),
             "passes_per_step": passes / args.steps,
@@ -310,10 +387,53 @@ def run_ours(args) -> None:
         }
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(1, 0)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "host")}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def step_shot_begin(step: int, rank: int, world: int, batch: int) -> int:
+    """First global shot of `rank`'s batch in `step`: every (step, rank) pair gets a
+    disjoint contiguous range, so each shot keeps its own for_shot(seed, shot) stream
+    (sim.py:54-57) and the union over ranks is [0, steps * world * batch)."""
+    return (step * world + rank) * batch
+
+
+def reduce_over_ranks(times: list, counts: list, device: str) -> tuple[list, list]:
+    """Times -> MAX over ranks (the job ends when the slowest rank does), counters ->
+    SUM over ranks; identity without a process group."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(times, dtype=torch.float64, device=device)
+    g = torch.tensor(counts, dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(g, op=dist.ReduceOp.SUM)
+    return t.tolist(), g.tolist()
+
+
+def relaunch(args, argv) -> int:
+    """`--gpus N` without a launcher: start N ranks (one per GPU) under torchrun."""
+    import socket
+
+    try:
+        import torch
+
+        visible = torch.cuda.device_count()
+    except Exception:  # pragma: no cover
+        visible = 0
+    if visible < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {visible} GPU(s) visible", file=sys.stderr)
+        return 1
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
 
 
 def main():
@@ -327,6 +447,8 @@ def main():
     ap.add_argument("--precision", choices=["c128", "c64"], default="c128")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args, sys.argv[1:]))
     if args.impl == "reference":
         run_reference(args)
     else:

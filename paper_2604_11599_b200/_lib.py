@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
 
 import numpy as np
@@ -210,10 +211,32 @@ class Context:
 _contexts: dict[int, Context] = {}
 
 
+def default_device() -> int:
+    """Device of a call that names none: $QSB_DEVICE, else the device torch was pointed
+    at (torch.cuda.set_device), else the launcher's LOCAL_RANK (one process per GPU under
+    torchrun), else 0.  Keeps `dist.sample_sharded(...)` without `device=` on its own
+    GPU per rank instead of piling every rank onto GPU 0."""
+    env = os.environ.get("QSB_DEVICE")
+    if env is not None:
+        return int(env)
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized() and torch.cuda.current_device() != 0:
+                return int(torch.cuda.current_device())
+        except Exception:  # pragma: no cover
+            pass
+    local = os.environ.get("LOCAL_RANK")
+    if local is not None:
+        n = device_count()
+        return int(local) % n if n > 0 else int(local)
+    return 0
+
+
 def context(device: int | None = None) -> Context:
     """Per-device default context (created lazily)."""
     if device is None:
-        device = int(os.environ.get("QSB_DEVICE", "0"))
+        device = default_device()
     ctx = _contexts.get(device)
     if ctx is None:
         ctx = Context(device)

@@ -24,11 +24,12 @@ def shard_bounds(total: int, world: int) -> list[tuple[int, int]]:
     return [(int(b[i]), int(b[i + 1])) for i in range(world)]
 
 
-def _world():
+def _world(group=None):
+    """(module, rank, world size) of `group` (default: the default process group)."""
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized():
-        return dist, dist.get_rank(), dist.get_world_size()
+        return dist, dist.get_rank(group), dist.get_world_size(group)
     return None, 0, 1
 
 
@@ -55,7 +56,7 @@ def sample_sharded(bound, shots: int, seed: int, *, executor=None, precision=Non
 
     if shots < 1:
         raise SimError("shots must be >= 1")
-    dist, rank, world = _world()
+    dist, rank, world = _world(group)
     lo, hi = shard_bounds(shots, world)[rank]
     if executor is None:
         local = _gpu_counts(bound, hi - lo, seed, lo, precision, device)
@@ -75,7 +76,7 @@ def observe_sharded(kernel, hamiltonian, points, *, executor=None, precision=Non
     """Energies of all points, computed as contiguous point ranges per rank and
     gathered in rank order (every rank returns the full array)."""
     pts = np.asarray(points, dtype=np.float64).reshape(len(points), -1)
-    dist, rank, world = _world()
+    dist, rank, world = _world(group)
     lo, hi = shard_bounds(len(pts), world)[rank]
     if hi > lo:
         if executor is None:

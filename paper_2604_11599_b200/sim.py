@@ -374,7 +374,7 @@ class Tape:
     """A compiled Kernel on one device context (qsb_tape)."""
 
     def __init__(self, kernel, ctx: _lib.Context):
-        self.kernel = kernel
+        # no reference to `kernel`: the cache entry dies with the kernel (compile_tape)
         self.ctx = ctx
         self.n = int(kernel.qubit_count)
         self.layout = [(n, int(w)) for n, w in kernel.classical_layout]
@@ -439,10 +439,16 @@ def compile_tape(kernel, device=None) -> Tape:
 
 
 class StateVector:
-    """Dense state, qubit k = index bit k.  `amps` is a host numpy view that is
-    downloaded on first access; after it is handed out, the host array is
-    authoritative and is re-uploaded before the next device operation (so in-place
-    edits by the caller are honoured, as with the reference's numpy buffer)."""
+    """Dense state, qubit k = index bit k, resident on the device.
+
+    `amps` downloads a host snapshot on first access and hands it out READ-ONLY, so a
+    caller that only reads it (every caller in the reference: suites.py, cli.py:104,
+    its tests) costs one download and no re-upload -- the device copy stays
+    authoritative.  Writing works as with the reference's numpy buffer (sim.py:80-95)
+    in two explicit ways: assign `state.amps = array`, or flip the snapshot's
+    `flags.writeable` back on and edit it in place; either way the host array is
+    uploaded before the next device operation.  An in-place write to the read-only
+    snapshot raises numpy's ValueError instead of being silently lost."""
 
     def __init__(self, n: int, amps: np.ndarray | None = None, *, precision=None, device=None):
         self.n = int(n)
@@ -453,6 +459,7 @@ class StateVector:
         self._h = h
         self._fin = weakref.finalize(self, self._ctx.lib.qsb_state_destroy, h)
         self._host = None
+        self._host_snapshot = False  # True: _host is an unmodified read-only download
         if amps is not None:
             a = np.ascontiguousarray(amps, dtype=np.complex128)
             if a.shape != (1 << self.n,):
@@ -465,18 +472,26 @@ class StateVector:
 
     # device sync ---------------------------------------------------------
     def _device(self):
-        """Handle with the device copy current (uploads a handed-out host view)."""
+        """Handle with the device copy current (uploads a handed-out host view that
+        the caller modified, or one that was assigned)."""
         if self._host is not None:
-            _lib.check(self._ctx.lib.qsb_state_set(self._h, _lib.ptr(self._host)))
+            if not self._host_snapshot or self._host.flags.writeable:
+                _lib.check(self._ctx.lib.qsb_state_set(self._h, _lib.ptr(np.ascontiguousarray(self._host))))
+                self.uploads += 1
             self._host = None
+            self._host_snapshot = False
         return self._h
+
+    uploads = 0  # host -> device state uploads (instrumentation for the tests)
 
     @property
     def amps(self) -> np.ndarray:
         if self._host is None:
             out = np.empty(1 << self.n, dtype=np.complex128)
             _lib.check(self._ctx.lib.qsb_state_get(self._h, _lib.ptr(out)))
+            out.flags.writeable = False
             self._host = out
+            self._host_snapshot = True
         return self._host
 
     @amps.setter
@@ -485,6 +500,7 @@ class StateVector:
         if a.shape != (1 << self.n,):
             raise SimError(f"amplitude vector of shape {a.shape} for {self.n} qubits")
         self._host = a
+        self._host_snapshot = False
 
     @property
     def precision(self) -> str:
