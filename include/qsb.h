@@ -165,6 +165,16 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
                                 const double* predrawn, int32_t predrawn_stride,
                                 uint64_t* bits_out, int32_t* shot_status);
 
+/* qsb_sample_trajectories (no pre-drawn stream) that also returns the final states of
+ * the first nstates shots into states_out[0..nstates-1] (tape qubit count, same
+ * precision), read from the batched streaming engine exactly as it left them (history
+ * dedup, fused passes, pending collapse applied): the final StateVector that
+ * run_trajectory (sim.py:306-314) returns for each of those shots.  Streaming engine
+ * only (QSB_ERR_UNSUPPORTED under the resident engine).                              */
+int32_t qsb_sample_trajectories_states(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
+                                       int64_t shot_begin, int64_t shot_count, uint64_t* bits_out,
+                                       int32_t* shot_status, int32_t nstates, qsb_state* states_out);
+
 /* run_trajectory (sim.py:306-314) for one shot.  The RNG starts from `rng_state`
  * (4 xoshiro256++ words, updated in place with the words after the run, like the
  * reference mutating its RngStream) or, when rng_state is null, from

@@ -101,6 +101,7 @@ _SIGS = {
     "qsb_tape_destroy": (_I32, [_P]),
     "qsb_tape_is_dynamic": (_I32, [_P, ctypes.POINTER(_I32)]),
     "qsb_sample_trajectories": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P, _I32, _P, _P]),
+    "qsb_sample_trajectories_states": (_I32, [_P, _I32, _P, _U64, _I64, _I64, _P, _P, _I32, _P]),
     "qsb_run_trajectory": (_I32, [_P, _I32, _P, _P, _U64, _I64, _P, _I32, _P, _P, _P, _I32, ctypes.POINTER(_I32),
                                   ctypes.POINTER(_I32)]),
     "qsb_statevector": (_I32, [_P, _P, _P]),

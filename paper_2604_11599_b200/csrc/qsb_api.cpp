@@ -1040,12 +1040,16 @@ namespace {
 // left on the device (dev_out, [shot_count][nwords]) for the device-side histogram.
 int sample_traj_impl(qsb_tape tp, int32_t precision, const double* params, uint64_t seed, int64_t shot_begin,
                      int64_t shot_count, const double* predrawn, int32_t predrawn_stride, uint64_t* bits_out,
-                     uint64_t* dev_out, int32_t* shot_status) {
+                     uint64_t* dev_out, int32_t* shot_status, int32_t nstates = 0, qsb_state* states = nullptr) {
   if (shot_count < 1) return fail(QSB_ERR_SIM, "shots must be >= 1");
   qsb_ctx ctx = tp->ctx;
   DeviceGuard g(ctx->device);
   const TapeInfo& t = tp->info;
   const int c64 = precision == QSB_C64 ? 1 : 0;
+  if (nstates < 0 || nstates > shot_count || (nstates && !states)) return fail(QSB_ERR_ARG, "bad nstates");
+  for (int32_t i = 0; i < nstates; ++i)
+    if (!states[i] || states[i]->n != t.n || states[i]->c64 != c64)
+      return fail(QSB_ERR_DIMENSION, "states_out shape / precision mismatch");
   QSB_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 32, ctx->stream));
   ctx->run_flops = 0;
   ctx->run_physical = false;
@@ -1067,6 +1071,7 @@ int sample_traj_impl(qsb_tape tp, int32_t precision, const double* params, uint6
   }
   std::vector<int32_t> status((size_t)shot_count, 0);
   if (use_resident(ctx, t, c64)) {
+    if (nstates) return fail(QSB_ERR_UNSUPPORTED, "final states of a batch: streaming engine only (engine=1)");
     QSB_CUDA(ctx->bits.ensure(sizeof(uint64_t) * t.nwords * shot_count));
     QSB_CUDA(ctx->status.ensure(sizeof(int32_t) * shot_count));
     ResidentArgs a{};
@@ -1110,6 +1115,15 @@ int sample_traj_impl(qsb_tape tp, int32_t precision, const double* params, uint6
                   nullptr, 0, nullptr};
       rc = run_stream(ctx, r);
       if (rc) return rc;
+      if (off == 0 && nstates) {  // the batch's first slots as the engine left them
+        StreamArgs a{};
+        a.state = ctx->state.p;
+        a.n = t.n;
+        a.c64 = c64;
+        a.ctl = ctx->ctl.as<TrajCtl>();
+        for (int32_t i = 0; i < nstates; ++i)
+          launch_finalize(a, states[i]->amps.p, r.final_clear, r.final_consumed, ctx->stream, i);
+      }
       QSB_CUDA(cudaMemcpyAsync(dev_out ? dev_out + off * t.nwords : bits_out + off * t.nwords, ctx->bits.p,
                                sizeof(uint64_t) * t.nwords * b,
                                dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
@@ -1150,6 +1164,13 @@ int32_t qsb_sample_trajectories(qsb_tape tp, int32_t precision, const double* pa
                                 int32_t predrawn_stride, uint64_t* bits_out, int32_t* shot_status) {
   return sample_traj_impl(tp, precision, params, seed, shot_begin, shot_count, predrawn, predrawn_stride, bits_out,
                           nullptr, shot_status);
+}
+
+int32_t qsb_sample_trajectories_states(qsb_tape tp, int32_t precision, const double* params, uint64_t seed,
+                                       int64_t shot_begin, int64_t shot_count, uint64_t* bits_out,
+                                       int32_t* shot_status, int32_t nstates, qsb_state* states_out) {
+  return sample_traj_impl(tp, precision, params, seed, shot_begin, shot_count, nullptr, 0, bits_out, nullptr,
+                          shot_status, nstates, states_out);
 }
 
 int32_t qsb_run_trajectory(qsb_tape tp, int32_t precision, const double* params, uint64_t* rng_state, uint64_t seed,

@@ -122,6 +122,6 @@ void launch_count_gates(const StreamArgs& a, const int32_t* guard_gates, int ngu
                         unsigned long long* out, cudaStream_t s);
 // out[i] = collapse(state[i ^ frame]) for slot 0; `clear` = frame bits already cleared by
 // passes after the last decide, `consumed` = a pass already applied the pending collapse
-void launch_finalize(const StreamArgs& a, void* out, uint64_t clear, int consumed, cudaStream_t s);
+void launch_finalize(const StreamArgs& a, void* out, uint64_t clear, int consumed, cudaStream_t s, int64_t slot = 0);
 
 }  // namespace qsb

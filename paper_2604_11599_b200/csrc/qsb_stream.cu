@@ -451,13 +451,14 @@ __global__ void k_count(StreamArgs a, const int32_t* guard_gates, int nguards, i
 }
 
 template <typename R>
-__global__ void k_finalize(StreamArgs a, typename Amp<R>::T* out, uint64_t clear, int consumed) {
+__global__ void k_finalize(StreamArgs a, typename Amp<R>::T* out, uint64_t clear, int consumed, int64_t slot) {
   using A = typename Amp<R>::T;
-  TrajCtl c = a.ctl[0];
+  TrajCtl c = a.ctl[slot];
   c.frame &= ~clear;
   if (consumed) c.pending = 0;
-  const A* st = reinterpret_cast<const A*>(a.state);
   const int64_t N = 1ll << a.n;
+  // the slot's state lives in its representative's buffer (history dedup; rep == slot without)
+  const A* st = reinterpret_cast<const A*>(a.state) + (int64_t)c.rep * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t p = (uint64_t)i ^ c.frame;
     A v = st[p];
@@ -543,12 +544,12 @@ void launch_count_gates(const StreamArgs& a, const int32_t* guard_gates, int ngu
   k_count<<<(unsigned)((a.slots + 127) / 128), 128, 0, s>>>(a, guard_gates, nguards, unguarded, out);
 }
 
-void launch_finalize(const StreamArgs& a, void* out, uint64_t clear, int consumed, cudaStream_t s) {
+void launch_finalize(const StreamArgs& a, void* out, uint64_t clear, int consumed, cudaStream_t s, int64_t slot) {
   int64_t N = 1ll << a.n;
   unsigned g = (unsigned)((N + 255) / 256);
   if (g > 148 * 32) g = 148 * 32;
-  if (a.c64) k_finalize<float><<<g, 256, 0, s>>>(a, (float2*)out, clear, consumed);
-  else k_finalize<double><<<g, 256, 0, s>>>(a, (double2*)out, clear, consumed);
+  if (a.c64) k_finalize<float><<<g, 256, 0, s>>>(a, (float2*)out, clear, consumed, slot);
+  else k_finalize<double><<<g, 256, 0, s>>>(a, (double2*)out, clear, consumed, slot);
 }
 
 }  // namespace qsb

@@ -705,6 +705,28 @@ def sample_words(bound, shots: int, seed: int, *, shot_begin: int = 0, precision
     return out, tape
 
 
+def sample_final_states(bound, shots: int, seed: int, nstates: int, *, shot_begin: int = 0, precision=None,
+                        device=None) -> tuple[np.ndarray, list]:
+    """`sample_words` of global shots [shot_begin, shot_begin + shots) through the batched
+    streaming engine, plus the final StateVector of the first `nstates` of those shots
+    as that engine left them (history dedup, fused passes, collapse applied) -- what
+    run_trajectory (sim.py:306-314) returns for each, for parity checks of the
+    production path at config size."""
+    if shots < 1:
+        raise SimError("shots must be >= 1")
+    tape = compile_tape(bound.kernel, device)
+    ctx = tape.ctx
+    pname = "c64" if _prec(precision) == _lib.C64 else "c128"
+    states = [StateVector(tape.n, precision=pname, device=ctx.device) for _ in range(nstates)]
+    handles = (ctypes.c_void_p * max(1, nstates))(*[st._h.value for st in states])
+    out = np.zeros((shots, tape.nwords), dtype=np.uint64)
+    status = np.zeros(shots, dtype=np.int32)
+    _lib.check(ctx.lib.qsb_sample_trajectories_states(tape.handle, _prec(precision), _lib.ptr(tape.params(bound.values)),
+                                                      int(seed) & _M64, int(shot_begin), int(shots), _lib.ptr(out),
+                                                      _lib.ptr(status), int(nstates), ctypes.cast(handles, ctypes.c_void_p)))
+    return out, states
+
+
 def histogram_from_words(tape: Tape, words: np.ndarray, shots: int) -> ShotHistogram:
     if tape.nbits == 0:
         return ShotHistogram({"": int(shots)}, int(shots))

@@ -343,12 +343,25 @@ def test_per_op_api_matches_reference_semantics():
     sim.apply_gate(st, Gate("x", (), (0,), ()))
     sim.reset(st, 0, sim.RngStream(0))
     np.testing.assert_allclose(st.amps, [1, 0], atol=1e-15)
-    # host edits of .amps are honoured by the next device op
+    # reading .amps hands out a read-only snapshot and costs no re-upload
     st = sim.StateVector.zero(1)
     a = st.amps
+    with pytest.raises(ValueError):
+        a[:] = [0, 1]
+    sim.apply_gate(st, Gate("h", (), (0,), ()))
+    assert st.uploads == 0
+    # explicit host edits are honoured by the next device op: in place after flipping
+    # the snapshot writeable, or by assignment
+    st = sim.StateVector.zero(1)
+    a = st.amps
+    a.flags.writeable = True
     a[:] = [0, 1]
     sim.apply_gate(st, Gate("x", (), (0,), ()))
     np.testing.assert_allclose(st.amps, [1, 0], atol=1e-15)
+    assert st.uploads == 1
+    st.amps = np.array([0, 1j])
+    sim.apply_gate(st, Gate("x", (), (0,), ()))
+    np.testing.assert_allclose(st.amps, [1j, 0], atol=1e-15)
     with pytest.raises(BadPauliString):
         sim.expval_pauli(st, "ZZ")
     with pytest.raises(BadPauliString):
