@@ -91,6 +91,8 @@ typedef struct {
 typedef struct qsb_ctx_s* qsb_ctx;
 typedef struct qsb_state_s* qsb_state;
 typedef struct qsb_tape_s* qsb_tape;
+typedef struct qsb_slicectl_s* qsb_slicectl;  /* classical control of one sliced trajectory */
+typedef struct qsb_comm_s* qsb_comm;          /* NCCL communicator of the sliced engine     */
 
 typedef struct {
   int64_t kernel_launches;   /* device kernels launched by the last run                   */
@@ -244,6 +246,53 @@ int32_t qsb_jit_nvrtc_version(int32_t* major, int32_t* minor);
  * blocks, host-check failures, pass flops per state unfused, the same fused}.          */
 int32_t qsb_fusion_stats(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
                          int32_t precision, int32_t reg_bits, double* out);
+
+/* ---- global-qubit-sliced engine (BASELINE cfg 5; sliced.py drives it) -----------------
+ * A state of n qubits is split into 2^G slices of L = n - G qubits (one per rank/GPU, or
+ * all on one GPU for the single-device emulation).  The host planner enqueues; every
+ * classical decision is made on the device from the qsb_slicectl (RNG stream, classical
+ * store, if/else guards, status), so a trajectory runs without host round-trips.
+ * Reference semantics: run_trajectory / _exec_ops (sim.py:279-314), measure / reset
+ * (sim.py:230-259), _eval_predicate (sim.py:262-276).                                  */
+/* RNG = rng_state (4 words) or RngStream.for_shot(seed, shot); nslices partial slots   */
+int32_t qsb_slice_ctl_create(qsb_ctx ctx, int32_t nslices, int32_t nbits, uint64_t seed, int64_t shot,
+                             const uint64_t* rng_state, qsb_slicectl* out);
+int32_t qsb_slice_ctl_destroy(qsb_slicectl c);
+/* synchronising read-back: classical words, qsb_status, uniforms drawn, RNG words     */
+int32_t qsb_slice_ctl_read(qsb_slicectl c, uint64_t* bits_out, int32_t* status, int32_t* draws, uint64_t* rng_out);
+/* IF (predicate evaluated on the device store at entry) / ELSE / ENDIF records         */
+int32_t qsb_slice_guard(qsb_slicectl c, const qsb_op* op);
+/* guarded gate on LOCAL positions (matrix host-built, has_matrix = 1; no swap)         */
+int32_t qsb_slice_gate(qsb_state st, qsb_slicectl c, const qsb_op* op);
+/* guarded complex scale (a diagonal gate on a global target, per slice)               */
+int32_t qsb_slice_scale(qsb_state st, qsb_slicectl c, double re, double im);
+/* this slice's partial p1 of local qubit `qubit` (< 0: its whole norm; select = 0: the
+ * slice holds none of the measured amplitudes) into partial slot `index`              */
+int32_t qsb_slice_prob1(qsb_state st, qsb_slicectl c, int32_t qubit, int32_t select, int32_t index);
+/* sum the partials in slice order, draw, decide (sim.py:236-248), write the bit       */
+int32_t qsb_slice_decide(qsb_slicectl c, int32_t kind, int32_t bit);
+/* apply the decision: local qubit (flip = reset) or, qubit < 0, a global qubit whose
+ * value in this slice is gbit                                                         */
+int32_t qsb_slice_collapse(qsb_state st, qsb_slicectl c, int32_t qubit, int32_t gbit, int32_t flip);
+/* single device: swap global position <-> local position pos between the slice pair
+ * (a: global bit 0, b: global bit 1) in place                                         */
+int32_t qsb_slice_exchange_local(qsb_state a, qsb_state b, int32_t pos);
+
+/* NCCL data plane (libnccl.so.2 opened at run time; QSB_ERR_UNSUPPORTED without it)    */
+int32_t qsb_comm_unique_id(uint8_t* out128);                  /* rank 0, broadcast by the caller */
+int32_t qsb_comm_init(qsb_ctx ctx, const uint8_t* id128, int32_t rank, int32_t nranks, qsb_comm* out);
+int32_t qsb_comm_destroy(qsb_comm c);
+int32_t qsb_comm_set_chunk(qsb_comm c, int64_t bytes);        /* exchange staging chunk (default 64 MiB) */
+/* partial slot `rank` of every rank -> all slots on every rank (ncclAllGather, in place) */
+int32_t qsb_comm_allgather_partials(qsb_comm c, qsb_slicectl s);
+/* exchange with `peer`: send the packed half of `send` (global bit send_c: local bit pos
+ * == !send_c) and unpack the peer's into the same half of `recv`; chunked ncclSend /
+ * ncclRecv on the context stream.  Production: send == recv (in place).               */
+int32_t qsb_comm_exchange(qsb_comm c, qsb_state send, int32_t send_c, qsb_state recv, int32_t recv_c, int32_t pos,
+                          int32_t peer);
+/* out3 = {bytes sent, exchanges, all-gathers}; CUDA-event ms of the last exchange     */
+int32_t qsb_comm_stats(qsb_comm c, int64_t* out3, double* last_exchange_ms);
+int32_t qsb_comm_nccl_version(int32_t* version);
 
 /* debug / known-answer hook: the first `count` uniforms of RngStream.for_shot(seed, shot)
  * drawn by the DEVICE generator (pins the on-device RNG to sim.py:54-72).              */

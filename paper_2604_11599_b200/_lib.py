@@ -118,6 +118,24 @@ _SIGS = {
     "qsb_state_prob1": (_I32, [_P, _I32, _PD]),
     "qsb_state_collapse": (_I32, [_P, _I32, _I32, _D, _I32]),
     "qsb_state_scale": (_I32, [_P, _D, _D]),
+    "qsb_slice_ctl_create": (_I32, [_P, _I32, _I32, _U64, _I64, _P, ctypes.POINTER(_P)]),
+    "qsb_slice_ctl_destroy": (_I32, [_P]),
+    "qsb_slice_ctl_read": (_I32, [_P, _P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), _P]),
+    "qsb_slice_guard": (_I32, [_P, _P]),
+    "qsb_slice_gate": (_I32, [_P, _P, _P]),
+    "qsb_slice_scale": (_I32, [_P, _P, _D, _D]),
+    "qsb_slice_prob1": (_I32, [_P, _P, _I32, _I32, _I32]),
+    "qsb_slice_decide": (_I32, [_P, _I32, _I32]),
+    "qsb_slice_collapse": (_I32, [_P, _P, _I32, _I32, _I32]),
+    "qsb_slice_exchange_local": (_I32, [_P, _P, _I32]),
+    "qsb_comm_unique_id": (_I32, [_P]),
+    "qsb_comm_init": (_I32, [_P, _P, _I32, _I32, ctypes.POINTER(_P)]),
+    "qsb_comm_destroy": (_I32, [_P]),
+    "qsb_comm_set_chunk": (_I32, [_P, _I64]),
+    "qsb_comm_allgather_partials": (_I32, [_P, _P]),
+    "qsb_comm_exchange": (_I32, [_P, _P, _I32, _P, _I32, _I32, _I32]),
+    "qsb_comm_stats": (_I32, [_P, _P, _PD]),
+    "qsb_comm_nccl_version": (_I32, [ctypes.POINTER(_I32)]),
 }
 
 EXPORTED = tuple(_SIGS)

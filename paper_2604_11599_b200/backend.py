@@ -7,9 +7,10 @@ routes every one of those references to this package's device simulator
 
 * `sys.modules["qasm2cudaq.sim"]` -> later `import qasm2cudaq.sim` / `from qasm2cudaq.sim
   import X` statements get the device module;
-* the attribute `sim` of `qasm2cudaq`, `qasm2cudaq.suites` and `qasm2cudaq.cli` (bound at
-  their import by `from . import sim`) and the names `qasm2cudaq/__init__.py` re-exports
-  (`qasm2cudaq.sample`, `qasm2cudaq.StateVector`, ...).
+* every binding of the reference simulator inside the loaded `qasm2cudaq.*` modules: the
+  attribute `sim` (`from . import sim`: `__init__`, `suites.py:21`, `cli.py:9`) and every
+  name bound from it (`from .sim import StateVector`: `__init__.py:23-35` re-exports,
+  `oracle.py`'s `isinstance(a, StateVector)` in `fidelity_up_to_global_phase`, ...).
 
 `install("cpu")` restores the reference module.  Nothing in the reference tree is edited;
 the switch is process-local.  `warm=True` creates the device context up front so the
@@ -23,9 +24,6 @@ import importlib
 import sys
 
 _SAVED: dict = {}
-# qasm2cudaq/__init__.py:23-35 re-exports these from .sim
-_REEXPORTS = ("ClassicalStore", "RngStream", "ShotHistogram", "StateVector", "apply_gate", "expval_pauli",
-              "measure", "reset", "run_trajectory", "sample", "statevector")
 
 
 def current() -> str:
@@ -37,10 +35,10 @@ def install(backend: str = "b200", *, warm: bool = True) -> None:
     if backend not in ("b200", "cpu"):
         raise ValueError(f"backend must be 'b200' or 'cpu', not {backend!r}")
     pkg = importlib.import_module("qasm2cudaq")
-    mods = [pkg] + [importlib.import_module(f"qasm2cudaq.{m}") for m in ("suites", "cli")]
+    for m in ("suites", "cli", "oracle"):  # load every module that binds sim names
+        importlib.import_module(f"qasm2cudaq.{m}")
     if not _SAVED:
         _SAVED["sim"] = sys.modules["qasm2cudaq.sim"]
-        _SAVED["names"] = {n: getattr(pkg, n) for n in _REEXPORTS if hasattr(pkg, n)}
     if backend == "b200":
         from . import sim as target
 
@@ -50,9 +48,17 @@ def install(backend: str = "b200", *, warm: bool = True) -> None:
             _lib.context()  # CUDA context + stream now, not inside the caller's first call
     else:
         target = _SAVED["sim"]
+    source = sys.modules["qasm2cudaq.sim"]
     sys.modules["qasm2cudaq.sim"] = target
-    for m in mods:
-        if hasattr(m, "sim"):
-            m.sim = target
-    for n in _REEXPORTS:
-        setattr(pkg, n, getattr(target, n))
+    # object identity -> name, for the functions / classes DEFINED by the module being
+    # replaced (not what it imported itself, e.g. kir.Gate or numpy)
+    by_id = {id(v): k for k, v in vars(source).items()
+             if not k.startswith("__") and getattr(v, "__module__", None) == source.__name__}
+    for name, mod in list(sys.modules.items()):
+        if mod is None or not (name == "qasm2cudaq" or name.startswith("qasm2cudaq.")) or mod in (source, target):
+            continue
+        for attr, val in list(vars(mod).items()):
+            if val is source:
+                setattr(mod, attr, target)
+            elif id(val) in by_id and hasattr(target, by_id[id(val)]) and not attr.startswith("__"):
+                setattr(mod, attr, getattr(target, by_id[id(val)]))

@@ -14,46 +14,20 @@
 #include "qsb_jit.h"
 #include "qsb_launch.h"
 #include "qsb_plan.h"
+#include "qsb_objects.h"
 
 using namespace qsb;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-int fail(int code, const std::string& msg) {
+int qsb::fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
 
-#define QSB_CUDA(call)                                                                         \
-  do {                                                                                         \
-    cudaError_t _e = (call);                                                                   \
-    if (_e != cudaSuccess) {                                                                   \
-      int _code = (_e == cudaErrorMemoryAllocation) ? QSB_ERR_OOM : QSB_ERR_CUDA;              \
-      return fail(_code, std::string(#call) + ": " + cudaGetErrorString(_e));                  \
-    }                                                                                          \
-  } while (0)
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  cudaError_t ensure(size_t want) {
-    if (want <= bytes && p) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&p, want ? want : 16);
-    if (e == cudaSuccess) bytes = want ? want : 16;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
-};
+namespace {
 
 struct PlanDev {
   StreamPlan plan;
@@ -67,28 +41,6 @@ struct PlanDev {
 
 }  // namespace
 
-struct qsb_ctx_s {
-  int device = 0;
-  int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-  std::vector<cudaEvent_t> pass_events;
-  int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
-  int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1, opt_lowq = 0;
-  DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
-  DevBuf shotwords, histo;  // device-side shot histogram (qsb_sample_counts)
-  qsb_stats last{};
-  double run_flops = 0;  // floating-point work of the pass kernels in the current run
-  bool run_physical = false;  // dedup ran: bytes / flops come from the device counters
-};
-
-struct qsb_state_s {
-  qsb_ctx ctx = nullptr;
-  int n = 0;
-  int c64 = 0;
-  DevBuf amps, scratch, tmp;
-};
-
 struct qsb_tape_s {
   qsb_ctx ctx = nullptr;
   TapeInfo info;
@@ -99,18 +51,6 @@ struct qsb_tape_s {
 
 namespace {
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 size_t amp_bytes(int c64) { return c64 ? 8 : 16; }
 

@@ -173,6 +173,21 @@ struct TrajCtl {
   int32_t pad2;
 };
 
+// classical control of one sliced trajectory (qsb_slice_*): everything a measurement,
+// reset or if/else decides lives here, in device memory -- the host only enqueues
+constexpr int kSliceWords = 16;  // classical bits of a sliced run: <= 1024
+struct SliceCtl {
+  uint64_t rng[4];
+  int32_t status;      // qsb_status (QSB_ERR_DEGENERATE once a branch had p < 1e-15)
+  int32_t depth, active;  // guard stack (counter form: active iff active == depth)
+  int32_t draws;       // uniforms consumed
+  int32_t outcome;     // last decision; -1: the measure / reset sat in an inactive branch
+  int32_t nwords;
+  double scale;        // 1 / sqrt(p_out) of the last decision
+  double p1;           // p1 of the last decision (sum of the per-slice partials, slice order)
+  uint64_t bits[kSliceWords];
+};
+
 // kernel arguments of the streaming engine (passed by value)
 struct StreamArgs {
   void* state;

@@ -124,4 +124,26 @@ void launch_count_gates(const StreamArgs& a, const int32_t* guard_gates, int ngu
 // passes after the last decide, `consumed` = a pass already applied the pending collapse
 void launch_finalize(const StreamArgs& a, void* out, uint64_t clear, int consumed, cudaStream_t s, int64_t slot = 0);
 
+// ---- global-qubit-sliced engine (qsb_slice.cu) ---------------------------------------
+void launch_slice_init(SliceCtl* c, uint64_t seed, int64_t shot, const uint64_t* rng_init, int nwords,
+                       cudaStream_t s);
+void launch_slice_guard(SliceCtl* c, int kind, int pred_bit, int pred_width, int pred_cmp, uint64_t rhs,
+                        cudaStream_t s);
+void launch_slice_gate(int c64, void* amps, int n, int t, uint64_t cm, uint64_t cv, int gc, const double* m,
+                       const SliceCtl* ctl, cudaStream_t s);
+void launch_slice_scale(int c64, void* amps, int n, double re, double im, const SliceCtl* ctl, cudaStream_t s);
+void launch_slice_put(const double* blocks, int nblocks, int select, double* partials, int index, cudaStream_t s);
+void launch_slice_decide(SliceCtl* c, const double* partials, int nslices, int kind, int bit, cudaStream_t s);
+void launch_slice_collapse(int c64, void* amps, int n, int q, int gbit, int flip, const SliceCtl* ctl,
+                           cudaStream_t s);
+void launch_slice_exchange_local(int c64, void* a, void* b, int n, int pos, cudaStream_t s);
+void launch_slice_pack(int c64, const void* amps, int pos, int c, int64_t first, int64_t count, void* out,
+                       cudaStream_t s);
+void launch_slice_unpack(int c64, void* amps, int pos, int c, int64_t first, int64_t count, const void* in,
+                         cudaStream_t s);
+// per-block partial sums of |a|^2 over the amplitudes with bit q set (q < 0: all); the
+// block count is prob_blocks_for(n, q)
+void launch_prob_blocks(int c64, const void* amps, int n, int q, double* blocks, cudaStream_t s);
+int prob_blocks_for(int n, int q);
+
 }  // namespace qsb

@@ -255,6 +255,14 @@ void launch_apply_swap(int c64, void* amps, int n, int t0, int t1, uint64_t cm, 
 
 int prob_scratch_len(int n) { return prob_blocks(n + 1); }
 
+int prob_blocks_for(int n, int q) { return q >= 0 ? prob_blocks(n) : prob_blocks(n + 1); }
+
+void launch_prob_blocks(int c64, const void* amps, int n, int q, double* blocks, cudaStream_t s) {
+  const int b = prob_blocks_for(n, q);
+  if (c64) k_prob_partial<float><<<b, kT, 0, s>>>((const float2*)amps, n, q, blocks);
+  else k_prob_partial<double><<<b, kT, 0, s>>>((const double2*)amps, n, q, blocks);
+}
+
 void launch_prob(int c64, const void* amps, int n, int q, double* scratch, double* out, cudaStream_t s) {
   int b = q >= 0 ? prob_blocks(n) : prob_blocks(n + 1);
   if (c64) k_prob_partial<float><<<b, kT, 0, s>>>((const float2*)amps, n, q, scratch);

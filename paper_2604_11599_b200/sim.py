@@ -506,6 +506,12 @@ class StateVector:
     def precision(self) -> str:
         return "c64" if self._prec == _lib.C64 else "c128"
 
+    def __array__(self, dtype=None, copy=None):
+        """numpy interop (`np.asarray(state)`): the amplitudes, as for callers that
+        treat a StateVector and an amplitude array alike (oracle.py:121-127)."""
+        a = self.amps
+        return a if dtype is None else a.astype(dtype)
+
     def norm(self) -> float:
         out = ctypes.c_double()
         _lib.check(self._ctx.lib.qsb_state_norm(self._device(), ctypes.byref(out)))

@@ -1,37 +1,44 @@
-"""Global-qubit slicing of one state vector over 2^G slices (BASELINE cfg 5:
-34 qubits complex128 over 8 B200s).
+"""Global-qubit slicing of one state vector over 2^G slices (BASELINE cfg 5: 34 qubits
+complex128 over 8 B200s).
 
 Layout.  The top G *physical* qubit positions are global: slice s holds the 2^L
-amplitudes (L = n - G) whose physical global bits equal `s ^ gframe`.  Logical qubit q
-lives at physical position perm[q].  One slice per rank (one GPU per process) in
-production; all slices in one process for the single-device emulation used by the
-tests.
+amplitudes (L = n - G) whose global physical bits equal s.  Logical qubit q lives at
+physical position perm[q].  One slice per rank (one GPU per process, NCCL between them)
+in production; all slices in one process for the single-device emulation.
 
-Operations (reference semantics: sim.py:203-259, 279-314):
-* gate with local targets: applied to every slice by the device kernels; controls on
-  global qubits select slices, controls on local qubits go to the kernel;
-* diagonal gate on a global target: a per-slice phase (folded into a diagonal gate on
-  a local control qubit when there is one);
-* non-diagonal gate on a global target: the global qubit is first swapped with the
-  top local position -- partner slices (s, s ^ bit) exchange one contiguous half of
-  their buffers (the only data movement: NCCL send/recv between GPUs, a device copy in
-  emulation) -- then applied locally;
-* swap gates are relabelings of `perm` (no data movement); X on a global qubit after
-  a reset flips `gframe`;
-* measure / reset: per-slice partial probabilities (deterministic device reductions)
-  summed in slice order -- identical on every rank -- then every rank draws the same
-  uniform from the same stream, so decisions agree without further communication.
+Plan (host, static, `plan_slices`).  The kernel IR is flattened (CondBlock -> IF / ELSE /
+ENDIF, sim.py:296-301) and the data movement is decided once, before anything runs:
+* a gate whose target is local runs on every slice (controls on global positions select
+  slices, local controls go to the kernel); a diagonal gate on a global target is a
+  per-slice phase;
+* a non-diagonal gate (or a reset) on a global position first EXCHANGES that global
+  position with a local one: the partner slices (s, s ^ bit) swap the halves in which the
+  local bit differs from their global bit (NCCL send/recv across GPUs, an in-place kernel
+  on one GPU).  The local position evicted is the one whose qubit is next needed locally
+  FARTHEST in the future (Belady look-ahead over the whole flattened program, branches
+  included) -- not a fixed position;
+* swap gates are relabelings of `perm` (no data movement).
+Because the plan does not depend on outcomes (a gate in an untaken branch still gets its
+exchange -- a relabeling that changes nothing logically), the host never has to wait for
+the device.
 
-The slice backend (device kernels) and the transport (exchange / all-gather) are
-injected; `GpuSliceBackend` + `LocalTransport` / `DistTransport` are the product
-paths.  Local gates between two exchanges / measurements run as one fused tape per
-slice (`GpuSliceBackend.flush`, C ABI `qsb_apply_tape`).
+Execution.  Every classical decision is made on the device (qsb_slice_*: SliceCtl with
+the RNG stream, the classical store and the if/else guards): a measurement writes each
+slice's partial p1 into a slot of a partials array, the transport all-gathers the slots
+(one 8-byte NCCL all-gather per measurement across ranks; nothing on one GPU), the decide
+kernel sums them IN SLICE ORDER on every rank, draws u from the shared stream and applies
+sim.py:230-259 (u < p1, p0 = 1 - p1, 1e-15, 1/sqrt); the collapse kernels read the
+decision.  The host reads the classical store back once, at the end.
+
+Backends: `GpuSliceBackend` (C ABI kernels).  Transports: `LocalTransport` (all slices in
+this process), `NcclTransport` (C ABI NCCL communicator: qsb_comm_*), `DistTransport`
+(torch.distributed: the protocol tests run it under gloo with a numpy backend).
 """
 
 from __future__ import annotations
 
 import ctypes
-import math
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -41,51 +48,192 @@ from .ir import op_kind
 _DIAG = frozenset(("z", "s", "t", "rz", "p"))
 
 
-class _G:  # minimal Gate stand-in for local application
-    __slots__ = ("base", "angles", "targets", "controls", "adjoint")
+# ---------------------------------------------------------------------------
+# static plan
+# ---------------------------------------------------------------------------
 
-    def __init__(self, base, targets, controls, adjoint=False, angles=()):
-        self.base, self.targets, self.controls, self.adjoint, self.angles = base, targets, controls, adjoint, angles
+
+@dataclass
+class SlicePlan:
+    n: int
+    G: int
+    steps: list = field(default_factory=list)  # see plan_slices
+    exchanges: int = 0
+    final_perm: list = field(default_factory=list)
+
+    @property
+    def L(self) -> int:
+        return self.n - self.G
+
+
+def _flatten(ops, out: list, offsets: dict, params) -> None:
+    from .sim import gate_matrix
+
+    for op in ops:
+        k = op_kind(op)
+        if k == "gate":
+            if op.base == "swap":
+                a, b = op.targets
+                if not op.controls:
+                    out.append(("swap", a, b))
+                    continue
+                # Fredkin = CX(b->a) . CCX(ctrls + a -> b) . CX(b->a)
+                x = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+                out.append(("gate", "x", x, a, ((b, 1),)))
+                out.append(("gate", "x", x, b, tuple(op.controls) + ((a, 1),)))
+                out.append(("gate", "x", x, a, ((b, 1),)))
+                continue
+            out.append(("gate", op.base, gate_matrix(op, params), op.targets[0], tuple(op.controls)))
+        elif k == "measure":
+            base, _ = offsets[op.bit[0]]
+            out.append(("measure", op.qubit, base + op.bit[1]))
+        elif k == "reset":
+            out.append(("reset", op.qubit))
+        elif k == "nop":
+            continue
+        else:
+            out.append(("if", op.predicate))
+            _flatten(op.then_body, out, offsets, params)
+            if op.else_body:
+                out.append(("else",))
+                _flatten(op.else_body, out, offsets, params)
+            out.append(("endif",))
+
+
+def _needs_local(item) -> int | None:
+    """Logical qubit the item needs at a local position, if any."""
+    if item[0] == "gate" and item[1] not in _DIAG:
+        return item[3]
+    if item[0] == "reset":
+        return item[1]
+    return None
+
+
+def plan_slices(kernel, params, G: int, lookahead: bool = True) -> SlicePlan:
+    """Static schedule of a sliced trajectory.  Steps (physical positions):
+        ("xchg", gpos, lpos)                         exchange a global with a local position
+        ("gate", base, m, tpos, ctrls, guarded)      ctrls: ((pos, pol), ...)
+        ("measure", pos, bit) / ("reset", pos)       reset positions are always local
+        ("if", pred_record) / ("else",) / ("endif",)
+    `lookahead=False` evicts the top local position every time (the round-1 rule)."""
+    from . import _lib
+    from .sim import _classical_offsets, _pred_record
+
+    n = int(kernel.qubit_count)
+    if not 0 <= G < n:
+        raise ValueError("need 0 <= G < n")
+    L = n - G
+    offsets = _classical_offsets([(nm, int(w)) for nm, w in kernel.classical_layout])
+    items: list = []
+    _flatten(kernel.body, items, offsets, params)
+    # next index at which each logical qubit must be local (Belady distances)
+    INF = len(items) + 1
+    next_need = [[INF] * n for _ in range(len(items) + 1)] if lookahead else None
+    if lookahead:
+        cur = [INF] * n
+        for i in range(len(items) - 1, -1, -1):
+            q = _needs_local(items[i])
+            if q is not None:
+                cur[q] = i
+            next_need[i] = list(cur)
+    perm = list(range(n))  # logical -> physical
+    where = list(range(n))  # physical -> logical
+    plan = SlicePlan(n, G)
+    depth = 0
+    for i, it in enumerate(items):
+        kind = it[0]
+        if kind == "swap":
+            a, b = it[1], it[2]
+            perm[a], perm[b] = perm[b], perm[a]
+            where[perm[a]], where[perm[b]] = a, b
+            continue
+        if kind == "if":
+            rec = np.zeros(1, dtype=_lib.OP_DTYPE)
+            _pred_record(rec[0], it[1], offsets)
+            plan.steps.append(("if", rec))
+            depth += 1
+            continue
+        if kind == "else":
+            plan.steps.append(("else",))
+            continue
+        if kind == "endif":
+            plan.steps.append(("endif",))
+            depth -= 1
+            continue
+        q = _needs_local(it)
+        if q is not None and perm[q] >= L:
+            busy = set()
+            if kind == "gate":
+                busy = {perm[c] for c, _ in it[4]}  # keep the gate's own controls local if possible
+            cands = [p for p in range(L)]
+            if lookahead:
+                nxt = next_need[i + 1] if i + 1 < len(items) else [INF] * n
+                cands.sort(key=lambda p: (nxt[where[p]], p not in busy, p), reverse=True)
+            else:
+                cands = [L - 1]
+            lpos = cands[0]
+            gpos = perm[q]
+            plan.steps.append(("xchg", gpos, lpos))
+            plan.exchanges += 1
+            ql = where[lpos]
+            perm[q], perm[ql] = lpos, gpos
+            where[lpos], where[gpos] = q, ql
+        if kind == "gate":
+            _, base, m, t, ctrls = it
+            plan.steps.append(("gate", base, m, perm[t], tuple((perm[c], pol) for c, pol in ctrls), depth > 0))
+        elif kind == "measure":
+            plan.steps.append(("measure", perm[it[1]], it[2]))
+        else:
+            plan.steps.append(("reset", perm[it[1]]))
+    plan.final_perm = perm
+    return plan
 
 
 # ---------------------------------------------------------------------------
-# backends
+# device backend (C ABI)
 # ---------------------------------------------------------------------------
 
 
 class GpuSliceBackend:
-    """Slices are device StateVectors on one GPU; kernels through the C ABI.
+    """Slices are device StateVectors; every primitive is an asynchronous C-ABI call on
+    the context's stream.  Unguarded local gates between two other steps are queued per
+    slice and run as ONE fused tape (`qsb_apply_tape`: the streaming engine's
+    register-blocked passes, in place) for slices of >= FUSE_MIN_LOCAL qubits; guarded
+    gates (inside an if/else) run one by one with the device guard check."""
 
-    Local gates are queued per slice and run as ONE fused tape (`qsb_apply_tape`: the
-    streaming engine's register-blocked passes, in place) when the slice is next
-    needed for anything else -- an exchange, a probability, a collapse, a scale or a
-    read -- so the gates between two exchanges cost a few state passes instead of one
-    pass each.  The fused tapes use the generic kernel (no per-tape NVRTC compile).
-    Small slices (the 1-GPU emulations) stay per-op: building a tape costs more than
-    a pass over them."""
-
-    # below this many local qubits a slice pass is cheaper than building a fused tape
-    # (tape + plan construction costs ~ms on the host)
-    FUSE_MIN_LOCAL = 24
+    FUSE_MIN_LOCAL = 24  # below: a slice pass is cheaper than building a fused tape
 
     def __init__(self, precision=None, device=None, fuse: bool | None = None):
         self.precision = precision
         self.device = device
-        self.fuse = fuse  # None: fuse slices of >= FUSE_MIN_LOCAL qubits
+        self.fuse = fuse
         self._queue: dict = {}  # id(slice) -> (slice, [qsb_op records])
+
+    @staticmethod
+    def _lib():
+        from . import _lib
+
+        return _lib
 
     def new_slice(self, L: int, initial_one: bool):
         from . import sim
 
         st = sim.StateVector.zero(L, precision=self.precision, device=self.device)
         if not initial_one:
-            self.scale(st, 0.0)
+            _l = self._lib()
+            _l.check(st._ctx.lib.qsb_state_scale(st._device(), 0.0, 0.0))
         return st
 
-    def flush(self, st=None) -> None:
-        """Run the queued gates of `st` (or of every slice) as one fused tape."""
-        from . import _lib
+    def new_ctl(self, nslices: int, nbits: int, rng_words, device_ctx=None):
+        _l = self._lib()
+        ctx = _l.context(self.device)
+        h = ctypes.c_void_p()
+        w = np.ascontiguousarray(rng_words, dtype=np.uint64)
+        _l.check(ctx.lib.qsb_slice_ctl_create(ctx.handle, nslices, nbits, 0, 0, _l.ptr(w), ctypes.byref(h)))
+        return _Ctl(ctx, h)
 
+    def flush(self, st=None) -> None:
+        _l = self._lib()
         keys = [id(st)] if st is not None else list(self._queue)
         for key in keys:
             item = self._queue.pop(key, None)
@@ -97,15 +245,16 @@ class GpuSliceBackend:
             tape = ctypes.c_void_p()
             ctx.set_option("jit", 0)
             try:
-                _lib.check(ctx.lib.qsb_tape_create(ctx.handle, _lib.ptr(ops), len(ops), sl.n, 0, 0, ctypes.byref(tape)))
+                _l.check(ctx.lib.qsb_tape_create(ctx.handle, _l.ptr(ops), len(ops), sl.n, 0, 0, ctypes.byref(tape)))
                 try:
-                    _lib.check(ctx.lib.qsb_apply_tape(tape, None, sl._device()))
+                    _l.check(ctx.lib.qsb_apply_tape(tape, None, sl._device()))
                 finally:
                     ctx.lib.qsb_tape_destroy(tape)
             finally:
                 ctx.set_option("jit", 1)
 
-    def apply(self, st, base, matrix, target, ctrl_local):
+    @staticmethod
+    def _record(base, m, t, ctrl_local):
         from . import _lib
 
         rec = np.zeros(1, dtype=_lib.OP_DTYPE)
@@ -113,68 +262,78 @@ class GpuSliceBackend:
         r["kind"] = _lib.OP_GATE
         r["base"] = _lib.BASES[base]  # selects the update class (perm / anti / diag / dense)
         r["ntargets"] = 1
-        r["target"][0] = target
+        r["target"][0] = t
         cm = cv = 0
         for q, pol in ctrl_local:
             cm |= 1 << q
             cv |= (1 << q) if pol else 0
         r["ctrl_mask"], r["ctrl_val"] = cm, cv
         r["angle_slot"][:] = -1
-        rec["mat"][0][:] = [matrix[0, 0].real, matrix[0, 0].imag, matrix[0, 1].real, matrix[0, 1].imag,
-                            matrix[1, 0].real, matrix[1, 0].imag, matrix[1, 1].real, matrix[1, 1].imag]
+        rec["mat"][0][:] = [m[0, 0].real, m[0, 0].imag, m[0, 1].real, m[0, 1].imag,
+                            m[1, 0].real, m[1, 0].imag, m[1, 1].real, m[1, 1].imag]
         rec["has_matrix"] = 1
-        if self.fuse or (self.fuse is None and st.n >= self.FUSE_MIN_LOCAL):
+        return rec
+
+    def gate(self, st, ctl, base, m, t, ctrl_local, guarded: bool):
+        rec = self._record(base, m, t, ctrl_local)
+        if not guarded and (self.fuse or (self.fuse is None and st.n >= self.FUSE_MIN_LOCAL)):
             self._queue.setdefault(id(st), (st, []))[1].append(rec)
             return
-        _lib.check(st._ctx.lib.qsb_apply_gate(st._device(), _lib.ptr(rec), None, 0))
+        self.flush(st)
+        _l = self._lib()
+        _l.check(st._ctx.lib.qsb_slice_gate(st._device(), ctl.h, _l.ptr(rec)))
 
-    def scale(self, st, c: complex):
-        from . import _lib
-
+    def scale(self, st, ctl, c: complex):
         self.flush(st)
         c = complex(c)
-        _lib.check(st._ctx.lib.qsb_state_scale(st._device(), c.real, c.imag))
+        self._lib().check(st._ctx.lib.qsb_slice_scale(st._device(), ctl.h, c.real, c.imag))
 
-    def prob1(self, st, q: int) -> float:
-        from . import _lib
+    def guard(self, ctl, kind: str, rec=None):
+        _l = self._lib()
+        if rec is None:
+            rec = np.zeros(1, dtype=_l.OP_DTYPE)
+            rec["kind"] = _l.OP_ELSE if kind == "else" else _l.OP_ENDIF
+        _l.check(ctl.ctx.lib.qsb_slice_guard(ctl.h, _l.ptr(rec)))
 
+    def prob1(self, st, ctl, q: int, select: bool, index: int):
         self.flush(st)
-        out = ctypes.c_double()
-        _lib.check(st._ctx.lib.qsb_state_prob1(st._device(), int(q), ctypes.byref(out)))
-        return float(out.value)
+        self._lib().check(st._ctx.lib.qsb_slice_prob1(st._device(), ctl.h, int(q), 1 if select else 0, int(index)))
 
-    def collapse(self, st, q, outcome, scale, flip):
-        from . import _lib
+    def decide(self, ctl, reset: bool, bit: int):
+        _l = self._lib()
+        _l.check(ctl.ctx.lib.qsb_slice_decide(ctl.h, _l.OP_RESET if reset else _l.OP_MEASURE, int(bit)))
 
+    def collapse(self, st, ctl, q: int, gbit: int, flip: bool):
         self.flush(st)
-        _lib.check(st._ctx.lib.qsb_state_collapse(st._device(), int(q), int(outcome), float(scale), int(flip)))
+        self._lib().check(st._ctx.lib.qsb_slice_collapse(st._device(), ctl.h, int(q), int(gbit), 1 if flip else 0))
 
-    def view(self, st):
-        """Zero-copy torch view (float64 / float32 pairs) of the slice's device buffer."""
-        import torch
+    def exchange_local(self, a, b, pos: int):
+        self.flush(a)
+        self.flush(b)
+        self._lib().check(a._ctx.lib.qsb_slice_exchange_local(a._device(), b._device(), int(pos)))
 
-        from . import _lib
-
-        self.flush(st)
-        ptr = ctypes.c_void_p()
-        _lib.check(st._ctx.lib.qsb_state_device_ptr(st._device(), ctypes.byref(ptr)))
-        st._ctx.synchronize()
-        c64 = st.precision == "c64"
-
-        class _Buf:
-            __cuda_array_interface__ = {"shape": (2 << st.n,), "typestr": "<f4" if c64 else "<f8",
-                                        "data": (ptr.value, False), "version": 3, "strides": None}
-
-        return torch.as_tensor(_Buf(), device=f"cuda:{st._ctx.device}")
-
-    def sync_after_transport(self, st):
-        import torch
-
-        torch.cuda.synchronize(st._ctx.device)
+    def read_ctl(self, ctl, nwords: int):
+        _l = self._lib()
+        bits = np.zeros(max(1, nwords), dtype=np.uint64)
+        rng = np.zeros(4, dtype=np.uint64)
+        status, draws = ctypes.c_int32(), ctypes.c_int32()
+        _l.check(ctl.ctx.lib.qsb_slice_ctl_read(ctl.h, _l.ptr(bits), ctypes.byref(status), ctypes.byref(draws),
+                                                _l.ptr(rng)))
+        return bits, int(status.value), int(draws.value), rng
 
     def to_numpy(self, st) -> np.ndarray:
         self.flush(st)
-        return st.amps.copy()
+        return np.array(st.amps)
+
+
+class _Ctl:
+    """Device SliceCtl handle (destroyed with the object)."""
+
+    def __init__(self, ctx, h):
+        import weakref
+
+        self.ctx, self.h = ctx, h
+        self._fin = weakref.finalize(self, ctx.lib.qsb_slice_ctl_destroy, h)
 
 
 # ---------------------------------------------------------------------------
@@ -183,29 +342,83 @@ class GpuSliceBackend:
 
 
 class LocalTransport:
-    """All slices in this process (single-device emulation of 2^G ranks)."""
+    """All slices in this process (single-device emulation of 2^G ranks): the partial
+    slots are already side by side, an exchange is an in-place kernel per slice pair."""
 
     def __init__(self, nslices: int):
         self.nslices = nslices
         self.owned = list(range(nslices))
 
-    def exchange(self, backend, slices, pairs):
-        """pairs: [(a, b)] where slice a sends/receives its upper half, b its lower."""
-        for a, b in pairs:
-            va, vb = backend.view(slices[a]), backend.view(slices[b])
-            h = va.numel() // 2
-            tmp = va[h:].clone()
-            va[h:].copy_(vb[:h])
-            vb[:h].copy_(tmp)
-            backend.sync_after_transport(slices[a])
+    def allgather(self, backend, ctl) -> None:
+        return None
 
-    def allgather_sum(self, values: dict) -> float:
-        return float(sum(values[s] for s in range(self.nslices)))
+    def exchange(self, backend, slices, pairs, lpos):
+        for a, b in pairs:
+            backend.exchange_local(slices[a], slices[b], lpos)
+
+
+class NcclTransport:
+    """One slice per rank; the C-ABI NCCL communicator (qsb_comm_*) on the context's
+    stream: exchanges are chunked ncclSend/ncclRecv of the packed halves, the partials an
+    in-place ncclAllGather.  The unique id is broadcast over the default
+    torch.distributed group (the only host-side collective, once)."""
+
+    def __init__(self, device=None, chunk_bytes: int | None = None):
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.rank, self.nslices = dist.get_rank(), dist.get_world_size()
+        self.owned = [self.rank]
+        self.ctx = _lib.context(device)
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            _lib.check(self.ctx.lib.qsb_comm_unique_id(_lib.ptr(uid)))
+        obj = [uid.tobytes()]
+        dist.broadcast_object_list(obj, src=0)
+        uid = np.frombuffer(obj[0], dtype=np.uint8).copy()
+        h = ctypes.c_void_p()
+        _lib.check(self.ctx.lib.qsb_comm_init(self.ctx.handle, _lib.ptr(uid), self.rank, self.nslices, ctypes.byref(h)))
+        self.h = h
+        if chunk_bytes:
+            _lib.check(self.ctx.lib.qsb_comm_set_chunk(h, int(chunk_bytes)))
+
+    def allgather(self, backend, ctl) -> None:
+        from . import _lib
+
+        _lib.check(self.ctx.lib.qsb_comm_allgather_partials(self.h, ctl.h))
+
+    def exchange(self, backend, slices, pairs, lpos):
+        from . import _lib
+
+        for a, b in pairs:
+            if self.rank not in (a, b):
+                continue
+            st = slices[self.rank]
+            backend.flush(st)
+            c = 0 if self.rank == a else 1
+            peer = b if self.rank == a else a
+            _lib.check(self.ctx.lib.qsb_comm_exchange(self.h, st._device(), c, st._device(), c, int(lpos), peer))
+
+    def stats(self) -> dict:
+        from . import _lib
+
+        out = np.zeros(3, dtype=np.int64)
+        ms = ctypes.c_double()
+        _lib.check(self.ctx.lib.qsb_comm_stats(self.h, _lib.ptr(out), ctypes.byref(ms)))
+        return {"bytes_sent": int(out[0]), "exchanges": int(out[1]), "allgathers": int(out[2]),
+                "last_exchange_ms": ms.value}
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.qsb_comm_destroy(self.h)
+            self.h = None
 
 
 class DistTransport:
-    """One slice per rank of the default torch.distributed group (NCCL on GPUs,
-    gloo for the CPU protocol tests)."""
+    """One slice per rank over torch.distributed (the protocol of NcclTransport with
+    host tensors: gloo in the CPU tests).  The backend provides `partials(ctl)` and
+    `pack` / `unpack` of a slice's exchanged half."""
 
     def __init__(self):
         import torch.distributed as dist
@@ -215,28 +428,30 @@ class DistTransport:
         self.nslices = dist.get_world_size()
         self.owned = [self.rank]
 
-    def exchange(self, backend, slices, pairs):
+    def allgather(self, backend, ctl) -> None:
+        import torch
+
+        part = backend.partials(ctl)
+        out = [torch.zeros(1, dtype=torch.float64) for _ in range(self.nslices)]
+        self.dist.all_gather(out, torch.tensor([float(part[self.rank])], dtype=torch.float64))
+        for s in range(self.nslices):
+            part[s] = float(out[s][0])
+
+    def exchange(self, backend, slices, pairs, lpos):
+        import torch
+
         dist = self.dist
         for a, b in pairs:
             if self.rank not in (a, b):
                 continue
-            me = self.rank
-            peer = b if me == a else a
-            v = backend.view(slices[me])
-            h = v.numel() // 2
-            half = v[h:] if me == a else v[:h]
-            tmp = half.clone()
-            ops = [dist.P2POp(dist.isend, tmp, peer), dist.P2POp(dist.irecv, half, peer)]
-            for r in dist.batch_isend_irecv(ops):
+            st = slices[self.rank]
+            c = 0 if self.rank == a else 1
+            peer = b if self.rank == a else a
+            send = torch.from_numpy(backend.pack(st, lpos, c).view(np.float64).copy())
+            recv = torch.empty_like(send)
+            for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, peer), dist.P2POp(dist.irecv, recv, peer)]):
                 r.wait()
-            backend.sync_after_transport(slices[me])
-
-    def allgather_sum(self, values: dict) -> float:
-        import torch
-
-        parts = [None] * self.nslices
-        self.dist.all_gather_object(parts, float(values[self.rank]))
-        return float(sum(parts))  # rank order
+            backend.unpack(st, lpos, c, recv.numpy().view(np.complex128))
 
 
 # ---------------------------------------------------------------------------
@@ -245,106 +460,18 @@ class DistTransport:
 
 
 class SlicedState:
+    """The slices owned by this process plus the layout (`perm`: logical qubit ->
+    physical position)."""
+
     def __init__(self, n: int, G: int, backend, transport):
-        if not 0 <= G < n:
-            raise ValueError("need 0 <= G < n")
         self.n, self.G, self.L = n, G, n - G
         self.backend, self.transport = backend, transport
-        self.perm = list(range(n))  # logical -> physical
-        self.gframe = 0
+        self.perm = list(range(n))
         self.slices = {s: backend.new_slice(self.L, s == 0) for s in transport.owned}
         self.exchanges = 0
 
-    # -- helpers --------------------------------------------------------------
-    def content(self, s: int) -> int:
-        return s ^ self.gframe
-
     def gbit(self, s: int, pos: int) -> int:
-        return (self.content(s) >> (pos - self.L)) & 1
-
-    def _swap_to_local(self, gpos: int) -> None:
-        """Exchange global position gpos with the top local position L-1."""
-        top = self.L - 1
-        bit = 1 << (gpos - self.L)
-        pairs = []
-        for s in range(2**self.G):
-            if self.content(s) & bit == 0:
-                partner = s ^ bit
-                pairs.append((s, partner))  # s keeps content bit 0: sends/receives its upper half
-        self.transport.exchange(self.backend, self.slices, pairs)
-        self.exchanges += 1
-        qa, qb = self.perm.index(gpos), self.perm.index(top)
-        self.perm[qa], self.perm[qb] = top, gpos
-
-    # -- operations ----------------------------------------------------------
-    def apply_gate(self, op, params=()) -> None:
-        from .sim import gate_matrix
-
-        base = op.base
-        if base == "swap":
-            a, b = op.targets
-            if not op.controls:
-                self.perm[a], self.perm[b] = self.perm[b], self.perm[a]
-                return
-            # Fredkin = CX(b->a) . CCX(ctrls, a -> b) . CX(b->a)
-            seq = [_G("x", (a,), ((b, 1),)), _G("x", (b,), tuple(op.controls) + ((a, 1),)), _G("x", (a,), ((b, 1),))]
-            for g in seq:
-                self.apply_gate(g)
-            return
-        m = gate_matrix(op, params)
-        t = self.perm[op.targets[0]]
-        if t >= self.L and base not in _DIAG:
-            self._swap_to_local(t)
-            t = self.perm[op.targets[0]]
-        ctrl = [(self.perm[q], pol) for q, pol in op.controls]
-        local = [(p, pol) for p, pol in ctrl if p < self.L]
-        glob = [(p, pol) for p, pol in ctrl if p >= self.L]
-        for s, st in self.slices.items():
-            if any(self.gbit(s, p) != pol for p, pol in glob):
-                continue
-            if t < self.L:
-                self.backend.apply(st, base, m, t, local)
-                continue
-            d = m[1, 1] if self.gbit(s, t) else m[0, 0]
-            if d == 1:
-                continue
-            if not local:
-                self.backend.scale(st, d)
-            else:  # phase on the first local control, the rest stay controls
-                (c, pol), rest = local[0], local[1:]
-                dm = np.array([[1, 0], [0, d]] if pol else [[d, 0], [0, 1]], dtype=np.complex128)
-                # a general diagonal ("rz" class): with pol = 0 the |0> entry is not 1
-                self.backend.apply(st, "rz", dm, c, rest)
-
-    def _p1(self, q: int) -> float:
-        p = self.perm[q]
-        vals = {}
-        for s, st in self.slices.items():
-            if p < self.L:
-                vals[s] = self.backend.prob1(st, p)
-            else:
-                vals[s] = self.backend.prob1(st, -1) if self.gbit(s, p) else 0.0
-        return self.transport.allgather_sum(vals)
-
-    def measure(self, q: int, rng, flip_if_one: bool = False) -> int:
-        """sim.py:230-259 on the sliced state (reset = flip_if_one)."""
-        p = self.perm[q]
-        p1 = self._p1(q)
-        u = rng.uniform()
-        outcome = 1 if u < p1 else 0
-        p_out = p1 if outcome == 1 else 1.0 - p1
-        if p_out < 1e-15:
-            raise DegenerateNorm(f"selected measurement branch {outcome} on qubit {q} has probability {p_out}")
-        scale = 1.0 / math.sqrt(p_out)
-        flip = flip_if_one and outcome == 1
-        for s, st in self.slices.items():
-            if p < self.L:
-                self.backend.collapse(st, p, outcome, scale, 1 if flip else 0)
-            else:
-                self.backend.scale(st, scale if self.gbit(s, p) == outcome else 0.0)
-        if flip and p >= self.L:
-            self.gframe ^= 1 << (p - self.L)
-        return outcome
+        return (s >> (pos - self.L)) & 1
 
     def gather(self) -> np.ndarray:
         """Logical amplitude vector (all slices must be local to this process)."""
@@ -352,7 +479,7 @@ class SlicedState:
         local_idx = np.arange(1 << self.L)
         for s, st in self.slices.items():
             a = self.backend.to_numpy(st)
-            phys = (self.content(s) << self.L) | local_idx
+            phys = (s << self.L) | local_idx
             logical = np.zeros_like(phys)
             for q in range(self.n):
                 logical |= ((phys >> self.perm[q]) & 1) << q
@@ -360,35 +487,82 @@ class SlicedState:
         return out
 
 
-def run_trajectory_sliced(bound, rng, global_qubits: int, *, backend=None, transport=None, trace=None):
-    """run_trajectory (sim.py:306-314) on a state sliced over 2^global_qubits slices."""
-    from .sim import ClassicalStore, _eval_predicate
+def execute(plan: SlicePlan, st: SlicedState, ctl) -> None:
+    """Enqueue a planned trajectory (nothing is read back)."""
+    be, tr, L = st.backend, st.transport, st.L
+    for step in plan.steps:
+        kind = step[0]
+        if kind == "gate":
+            _, base, m, t, ctrls, guarded = step
+            local = [(p, pol) for p, pol in ctrls if p < L]
+            glob = [(p, pol) for p, pol in ctrls if p >= L]
+            for s, sl in st.slices.items():
+                if any(st.gbit(s, p) != pol for p, pol in glob):
+                    continue
+                if t < L:
+                    be.gate(sl, ctl, base, m, t, local, guarded)
+                    continue
+                d = m[1, 1] if st.gbit(s, t) else m[0, 0]  # diagonal on a global target
+                if d == 1:
+                    continue
+                if not local:
+                    be.scale(sl, ctl, d)
+                else:  # a phase on the first local control, the rest stay controls
+                    (c, pol), rest = local[0], local[1:]
+                    dm = np.array([[1, 0], [0, d]] if pol else [[d, 0], [0, 1]], dtype=np.complex128)
+                    be.gate(sl, ctl, "rz", dm, c, rest, guarded)
+        elif kind in ("measure", "reset"):
+            p = step[1]
+            for s, sl in st.slices.items():
+                if p < L:
+                    be.prob1(sl, ctl, p, True, s)
+                else:
+                    be.prob1(sl, ctl, -1, st.gbit(s, p) == 1, s)
+            tr.allgather(be, ctl)
+            be.decide(ctl, kind == "reset", step[2] if kind == "measure" else 0)
+            for s, sl in st.slices.items():
+                if p < L:
+                    be.collapse(sl, ctl, p, 0, kind == "reset")
+                else:
+                    be.collapse(sl, ctl, -1, st.gbit(s, p), False)
+        elif kind == "xchg":
+            _, gpos, lpos = step
+            bit = 1 << (gpos - L)
+            pairs = [(s, s ^ bit) for s in range(1 << st.G) if not s & bit]
+            tr.exchange(be, st.slices, pairs, lpos)
+            st.exchanges += 1
+        elif kind == "if":
+            be.guard(ctl, "if", step[1])
+        else:
+            be.guard(ctl, kind)
+    if hasattr(be, "flush"):
+        be.flush()
+    st.perm = list(plan.final_perm)
+
+
+def run_trajectory_sliced(bound, rng, global_qubits: int, *, backend=None, transport=None, lookahead: bool = True,
+                          plan: SlicePlan | None = None):
+    """run_trajectory (sim.py:306-314) on a state sliced over 2^global_qubits slices.
+    `rng` must be an xoshiro stream (RngStream, ours or the reference's); it is advanced
+    by exactly the uniforms consumed.  Returns (ClassicalStore, SlicedState)."""
+    from .sim import ClassicalStore, _rng_words
 
     k = bound.kernel
     n = int(k.qubit_count)
     backend = backend or GpuSliceBackend()
     transport = transport or LocalTransport(2**global_qubits)
+    if plan is None:
+        plan = plan_slices(k, bound.values, global_qubits, lookahead=lookahead)
+    words = _rng_words(rng)
+    if words is None:
+        raise ValueError("the sliced engine draws on the device: pass an RngStream")
+    layout = [(nm, int(w)) for nm, w in k.classical_layout]
+    nbits = sum(w for _, w in layout)
     st = SlicedState(n, global_qubits, backend, transport)
-    store = ClassicalStore(k.classical_layout)
-
-    def run(ops):
-        for op in ops:
-            kind = op_kind(op)
-            if kind == "gate":
-                st.apply_gate(op, bound.values)
-            elif kind == "measure":
-                store.write_bit(op.bit[0], op.bit[1], st.measure(op.qubit, rng))
-            elif kind == "reset":
-                st.measure(op.qubit, rng, flip_if_one=True)
-            elif kind == "nop":
-                continue
-            else:
-                taken = _eval_predicate(op.predicate, store)
-                if trace is not None:
-                    trace.append((op.predicate, {nm: list(b) for nm, b in store.bits.items()}, taken))
-                run(op.then_body if taken else op.else_body)
-
-    run(k.body)
-    if hasattr(backend, "flush"):
-        backend.flush()
-    return store, st
+    ctl = backend.new_ctl(2**global_qubits, nbits, words)
+    execute(plan, st, ctl)
+    bits, status, _draws, rng_words = backend.read_ctl(ctl, max(1, (nbits + 63) // 64))
+    rng.s0, rng.s1, rng.s2, rng.s3 = (int(w) for w in rng_words)
+    if status:
+        raise DegenerateNorm("selected measurement branch has probability < 1e-15")
+    return ClassicalStore._from_words(layout, bits), st
