@@ -19,3 +19,7 @@ backend.install(os.environ.get("QSB_BACKEND", "b200"))
 
 def pytest_report_header(config):
     return f"qasm2cudaq.sim backend: {backend.current()}"
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    terminalreporter.write_line(f"qasm2cudaq.sim backend: {backend.current()}")
