@@ -719,7 +719,8 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   if (groups.empty()) groups.push_back({lowmask, {}});
   for (int t : diag) groups[0].terms.push_back(t);
   std::vector<ExpvalTerm> dev_terms, by_out(nterm);
-  std::vector<ExpvalGroup> dev_groups;
+  std::vector<ExpvalGroup> dev_groups;  // pair-loop launches (path 1)
+  std::vector<ExpvalGroup> acc_groups;  // accumulating launches (path 0, k = 12)
   std::vector<EvMap> dev_maps;
   const int sb = c64 ? 4 : 3;
   for (Grp& g : groups) {
@@ -769,8 +770,21 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
           }
         if (!placed) maps.push_back({xl, {t}});
       }
-      eg.map_begin = (int)dev_maps.size();
-      eg.nmap = (int)maps.size();
+      // per mapping: the terms sorted by (register X pattern, Re / Im) so that each class
+      // of equal patterns is one run (its pair products are formed once), then cut into
+      // launches of <= kEvAccTerms terms (the per-thread accumulators of one launch live
+      // in shared memory: kEvAccTerms x 256 doubles)
+      auto flush_launch = [&](ExpvalGroup& cur) {
+        if (cur.nterm) acc_groups.push_back(cur);
+        cur = ExpvalGroup{};
+        cur.smask = g.S;
+        cur.k = k;
+        cur.lowq = lowq;
+        cur.term_begin = (int)dev_terms.size();
+        cur.map_begin = (int)dev_maps.size();
+      };
+      ExpvalGroup cur{};
+      flush_launch(cur);
       for (Map& m : maps) {
         int rpos[4], nr = 0;
         for (int p = 0; p < k && nr < 4; ++p)
@@ -779,8 +793,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
           if (!(m.U >> p & 1)) rpos[nr++] = p;
         EvMap em{};
         tile_mapping(rpos, 4, k, sb, em.tpos, em.soff);
-        em.term_begin = (int)dev_terms.size();
-        em.nterm = (int)m.terms.size();
+        std::vector<ExpvalTerm> mts;
         for (int t : m.terms) {
           ExpvalTerm e = make_term(t);
           for (int b = 0; b < 4; ++b)
@@ -791,37 +804,60 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
               if (j >> b & 1) pos |= 1u << rpos[b];
             if (__builtin_popcount(pos & e.zl) & 1) e.zsig |= 1u << j;
           }
-          dev_terms.push_back(e);
-          by_out[t] = e;
+          e.path = 0;
+          mts.push_back(e);
         }
-        dev_maps.push_back(em);
-      }
-      eg.nterm = (int)dev_terms.size() - eg.term_begin;
-      if (!wide.empty()) {
-        if (eg.nterm) dev_groups.push_back(eg);
-        eg = ExpvalGroup{};
-        eg.smask = g.S;
-        eg.k = k;
-        eg.lowq = lowq;
-        eg.term_begin = (int)dev_terms.size();
-        eg.nterm = (int)wide.size();
-        for (int t : wide) {
-          ExpvalTerm e = make_term(t);
-          dev_terms.push_back(e);
-          by_out[t] = e;
+        std::stable_sort(mts.begin(), mts.end(), [](const ExpvalTerm& x, const ExpvalTerm& y) {
+          return x.xr != y.xr ? x.xr < y.xr : (x.ny & 1) < (y.ny & 1);
+        });
+        size_t i = 0;
+        while (i < mts.size()) {
+          if (cur.nterm == kEvAccTerms) flush_launch(cur);
+          const size_t take = std::min<size_t>(mts.size() - i, (size_t)(kEvAccTerms - cur.nterm));
+          EvMap part = em;
+          part.term_begin = (int)dev_terms.size();
+          part.nterm = (int)take;
+          for (size_t j = 0; j < take; ++j) {
+            dev_terms.push_back(mts[i + j]);
+            by_out[mts[i + j].out] = mts[i + j];
+          }
+          dev_maps.push_back(part);
+          cur.nterm += (int)take;
+          cur.nmap++;
+          i += take;
         }
       }
-    } else {
-      for (int t : g.terms) {
+      flush_launch(cur);
+      eg = ExpvalGroup{};
+      eg.smask = g.S;
+      eg.k = k;
+      eg.lowq = lowq;
+      eg.term_begin = (int)dev_terms.size();
+      eg.nterm = (int)wide.size();
+      for (int t : wide) {
         ExpvalTerm e = make_term(t);
+        e.path = 1;
         dev_terms.push_back(e);
         by_out[t] = e;
       }
+      if (eg.nterm) dev_groups.push_back(eg);
+    } else {
+      for (int t : g.terms) {
+        ExpvalTerm e = make_term(t);
+        e.path = 1;
+        dev_terms.push_back(e);
+        by_out[t] = e;
+      }
+      dev_groups.push_back(eg);
     }
-    dev_groups.push_back(eg);
   }
   const int ntl = n - k;
-  const size_t pbytes = sizeof(double) * (size_t)slots * nterm * ((size_t)1 << ntl);
+  const int nchunks = expval_acc_chunks(n);
+  const bool any_tile = !dev_groups.empty();
+  // partials: [slot][chunk][term] of the accumulating kernel, then (pair-loop terms only)
+  // [slot][tile][term]
+  const size_t acc_words = (size_t)slots * nterm * nchunks;
+  const size_t pbytes = sizeof(double) * (acc_words + (any_tile ? (size_t)slots * nterm * ((size_t)1 << ntl) : 0));
   QSB_CUDA(ctx->misc.ensure(pbytes + 64));
   QSB_CUDA(ctx->misc2.ensure(sizeof(ExpvalTerm) * 2 * (nterm + 1) + sizeof(double) * nterm * slots +
                               sizeof(EvMap) * (dev_maps.size() + 1) + 64));
@@ -838,11 +874,15 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
                              ctx->stream));
     QSB_CUDA(cudaMemcpyAsync(d_byout, by_out.data(), sizeof(ExpvalTerm) * nterm, cudaMemcpyHostToDevice, ctx->stream));
   }
+  double* p_acc = ctx->misc.as<double>();
+  double* p_tile = p_acc + acc_words;
+  for (const ExpvalGroup& g : acc_groups)
+    launch_expval_acc(c64, amps, n, slots, g, d_terms, d_maps, p_acc, nterm, ctx->stream);
   for (const ExpvalGroup& g : dev_groups)
     if (g.nterm)
-      launch_expval_tile(c64, amps, n, slots, g, d_terms, d_maps, ctx->misc.as<double>(), nterm, ctx->stream);
+      launch_expval_tile(c64, amps, n, slots, g, d_terms, d_maps, p_tile, nterm, ctx->stream);
   QSB_CUDA(cudaGetLastError());
-  launch_expval_tile_finish(ctx->misc.as<double>(), slots, nterm, ntl, d_byout, d_out, ctx->stream);
+  launch_expval_tile_finish(p_acc, nchunks, p_tile, 1 << ntl, slots, nterm, d_byout, d_out, ctx->stream);
   QSB_CUDA(cudaMemcpyAsync(out_host, d_out, sizeof(double) * nterm * slots, cudaMemcpyDeviceToHost, ctx->stream));
   QSB_CUDA(cudaStreamSynchronize(ctx->stream));
   return check_sticky();

@@ -288,20 +288,185 @@ __global__ void __launch_bounds__(kET, 2) k_expval_reg(const typename Amp<R>::T*
   }
 }
 
-// partial layout [slot][tile][term]: consecutive threads (terms) read consecutive words
-__global__ void k_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
-                                     const ExpvalTerm* terms_by_out, double* out) {
+// partials: the accumulating kernel's [slot][chunk][term] (path 0) or the pair-loop
+// kernel's [slot][tile][term] (path 1); consecutive threads (terms) read consecutive
+// words; chunks / tiles summed in order (deterministic)
+__global__ void k_expval_tile_finish(const double* pacc, int nchunks, const double* ptile, int ntiles, int64_t slots,
+                                     int nterm, const ExpvalTerm* terms_by_out, double* out) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= slots * nterm) return;
   const int t = (int)(idx % nterm);
   const int64_t slot = idx / nterm;
-  const int64_t tiles = (int64_t)1 << ntiles_log2;
-  const double* p = partial + slot * tiles * nterm + t;
-  double s = 0.0;
-  for (int64_t b = 0; b < tiles; ++b) s += p[b * nterm];
   const ExpvalTerm tm = terms_by_out[t];
+  const int cnt = tm.path ? ntiles : nchunks;
+  const double* p = (tm.path ? ptile : pacc) + slot * cnt * nterm + t;
+  double s = 0.0;
+  for (int64_t b = 0; b < cnt; ++b) s += p[b * nterm];
   if (tm.xg | tm.xl) s *= 2.0;
   out[idx] = ((tm.ny & 3) >= 2) ? -s : s;
+}
+
+// ---- per-thread accumulating kernel (k = 12; the cfg 3 hot path) ---------------------
+//
+// One CTA = one (state, chunk of consecutive tiles).  Tiles are double-buffered with
+// cp.async; per register mapping every thread loads its 16 amplitudes, and per CLASS of
+// terms (same register X pattern XR) it forms the 8 pair products conj(v_j) v_{j^XR}
+// once; each term of the class is then 8 signed adds of their real or imaginary parts
+// (16 for the diagonal class, of |v_j|^2), signed by the thread's and the tile's Z
+// parity, and ADDED TO THE THREAD'S OWN ACCUMULATOR for that term in shared memory.  No
+// cross-thread reduction happens per tile: one fixed-order reduction per CTA at the end.
+// Partials [state][chunk][term] are summed over chunks in order by the finish kernel --
+// deterministic, and independent of how many states a launch holds.
+
+template <typename R, int XR>
+__device__ __forceinline__ void ev_class(const typename Amp<R>::T* v, const ExpvalTerm* st, int t0, int t1,
+                                         double* acc, int tid, uint32_t tb, uint64_t base) {
+  constexpr int TOP = XR ? 1 << (31 - __builtin_clz(XR)) : 0;
+  if (XR == 0) {
+    R nv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) nv[j] = fma(v[j].x, v[j].x, v[j].y * v[j].y);
+    for (int t = t0; t < t1; ++t) {
+      const ExpvalTerm& tm = st[t];
+      R s = (R)0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) s += flip_sign(nv[j], tm.zsig, j);
+      const uint32_t par = (__popc(tb & tm.zl) + __popcll(base & tm.zg)) & 1;
+      acc[t * kET + tid] += flip_sign((double)s, par, 0);
+    }
+    return;
+  }
+  R pr[8], pi[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int j = ((k & ~(TOP - 1)) << 1) | (k & (TOP - 1));  // k with a 0 inserted at TOP
+    const R ur = v[j].x, ui = v[j].y, vr = v[j ^ XR].x, vi = v[j ^ XR].y;
+    pr[k] = fma(ur, vr, ui * vi);
+    pi[k] = fma(ur, vi, -ui * vr);
+  }
+  for (int t = t0; t < t1; ++t) {
+    const ExpvalTerm& tm = st[t];
+    R s = (R)0;
+    if (tm.ny & 1) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += flip_sign(pi[k], tm.zsig, ((k & ~(TOP - 1)) << 1) | (k & (TOP - 1)));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += flip_sign(pr[k], tm.zsig, ((k & ~(TOP - 1)) << 1) | (k & (TOP - 1)));
+    }
+    const uint32_t par = (__popc(tb & tm.zl) + __popcll(base & tm.zg)) & 1;
+    acc[t * kET + tid] += flip_sign((double)s, par, 0);
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ void ev_class_dispatch(int xr, const typename Amp<R>::T* v, const ExpvalTerm* st, int t0,
+                                                  int t1, double* acc, int tid, uint32_t tb, uint64_t base) {
+  switch (xr) {
+#define QSB_EV_CLS(X) \
+  case X: ev_class<R, X>(v, st, t0, t1, acc, tid, tb, base); break;
+    QSB_EV_CLS(0) QSB_EV_CLS(1) QSB_EV_CLS(2) QSB_EV_CLS(3) QSB_EV_CLS(4) QSB_EV_CLS(5) QSB_EV_CLS(6) QSB_EV_CLS(7)
+    QSB_EV_CLS(8) QSB_EV_CLS(9) QSB_EV_CLS(10) QSB_EV_CLS(11) QSB_EV_CLS(12) QSB_EV_CLS(13) QSB_EV_CLS(14)
+    QSB_EV_CLS(15)
+#undef QSB_EV_CLS
+    default: break;
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kET, 1) k_expval_acc(const typename Amp<R>::T* __restrict__ states, int n,
+                                                      ExpvalGroup g, const ExpvalTerm* __restrict__ terms,
+                                                      const EvMap* __restrict__ maps, double* __restrict__ partial,
+                                                      int nterm_total, int nchunks) {
+  using A = typename Amp<R>::T;
+  constexpr int SB = sizeof(R) == 8 ? 3 : 4;
+  constexpr int K = 12, TL = 1 << K;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* tiles = reinterpret_cast<A*>(smem_raw);                              // [2][TL]
+  double* acc = reinterpret_cast<double*>(tiles + 2 * TL);                // [nterm][kET]
+  uint64_t* hi_off = reinterpret_cast<uint64_t*>(acc + g.nterm * kET);    // [TL >> lowq]
+  uint32_t* swz = reinterpret_cast<uint32_t*>(hi_off + (TL >> g.lowq));   // [TL >> SB]
+  ExpvalTerm* sterm = reinterpret_cast<ExpvalTerm*>(
+      (reinterpret_cast<size_t>(swz + (TL >> SB)) + 15) & ~(size_t)15);  // [nterm]
+  EvMap* smap = reinterpret_cast<EvMap*>(sterm + g.nterm);                // [nmap]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t qmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  const uint64_t lowm = (1ull << g.lowq) - 1;
+  const uint64_t shi = g.smask & ~lowm;
+  for (int h = tid; h < (TL >> g.lowq); h += kET) hi_off[h] = pdep64((uint64_t)h, shi);
+  const uint8_t* V = SB == 3 ? c_swz3 : c_swz4;
+  for (int h = tid; h < (TL >> SB); h += kET) {
+    uint32_t sw = 0;
+    for (int p = SB, hh = h; hh; ++p, hh >>= 1)
+      if (hh & 1) sw ^= V[p];
+    swz[h] = sw;
+  }
+  for (int t = tid; t < g.nterm; t += kET) sterm[t] = terms[g.term_begin + t];
+  for (int m = tid; m < g.nmap; m += kET) smap[m] = maps[g.map_begin + m];
+  for (int i = tid; i < g.nterm * kET; i += kET) acc[i] = 0.0;
+  __syncthreads();
+  const int ntl = n - K;
+  const int64_t ntiles = (int64_t)1 << ntl;
+  const int64_t slot = blockIdx.x / nchunks, chunk = blockIdx.x % nchunks;
+  const int64_t tpc = ntiles / nchunks, w0 = chunk * tpc;
+  const uint64_t outmask = ~g.smask & qmask;
+  const A* st = states + (slot << n);
+  const uint64_t Pt = ((uint64_t)tid & lowm) | hi_off[tid >> g.lowq];
+  const uint32_t St = swz_slot<SB>(swz, (uint32_t)tid);
+  const int hstep = kET >> g.lowq;
+  auto load = [&](int64_t w, A* dst_tile) {
+    const uint64_t base = pdep64((uint64_t)w, outmask);
+#pragma unroll
+    for (int i = 0; i < TL / kET; ++i) {
+      const A* src = st + (base | Pt | hi_off[i * hstep]);
+      A* dst = dst_tile + (St ^ swz_slot<SB>(swz, (uint32_t)(i * kET)));
+      if (sizeof(A) == 16) cp_async16(dst, src);
+      else cp_async8(dst, src);
+    }
+    cp_async_commit();
+  };
+  load(w0, tiles);
+  for (int64_t i = 0; i < tpc; ++i) {
+    if (i + 1 < tpc) {
+      load(w0 + i + 1, tiles + ((i + 1) & 1) * TL);
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();
+    const A* tile = tiles + (i & 1) * TL;
+    const uint64_t base = pdep64((uint64_t)(w0 + i), outmask);
+    for (int mi = 0; mi < g.nmap; ++mi) {
+      const EvMap& m = smap[mi];
+      uint32_t tb = 0;
+#pragma unroll
+      for (int b = 0; b < K - 4; ++b) tb |= (uint32_t)((tid >> b) & 1) << m.tpos[b];
+      const uint32_t sbase = swz_slot<SB>(swz, tb);
+      A v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = tile[sbase ^ m.soff[j]];
+      const int tend = m.term_begin - g.term_begin + m.nterm;
+      for (int t = m.term_begin - g.term_begin; t < tend;) {  // classes: runs of equal xr
+        const uint32_t xr = sterm[t].xr;
+        int e = t + 1;
+        while (e < tend && sterm[e].xr == xr) ++e;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) opaque(v[j]);  // no hoisting of every class's products
+        ev_class_dispatch<R>((int)xr, v, sterm, t, e, acc, tid, tb, base);
+        t = e;
+      }
+    }
+    __syncthreads();  // the buffer is refilled by the load issued next iteration
+  }
+  // one fixed-order reduction per CTA: warp w sums terms w, w + 8, ...; lane l adds the
+  // accumulators of threads l, l + 32, ... in order, then a fixed shuffle tree
+  for (int t = warp; t < g.nterm; t += kET / 32) {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < kET / 32; ++r) s += acc[t * kET + r * 32 + lane];
+    for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) partial[(slot * nchunks + chunk) * nterm_total + sterm[t].out] = s;
+  }
 }
 
 }  // namespace
@@ -363,11 +528,43 @@ void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const
   }
 }
 
-void launch_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
-                               const ExpvalTerm* terms_by_out, double* out, cudaStream_t s) {
+void launch_expval_tile_finish(const double* partial_acc, int nchunks, const double* partial_tile, int ntiles,
+                               int64_t slots, int nterm, const ExpvalTerm* terms_by_out, double* out, cudaStream_t s) {
   const int64_t items = slots * nterm;
-  k_expval_tile_finish<<<(unsigned)((items + 127) / 128), 128, 0, s>>>(partial, slots, nterm, ntiles_log2,
-                                                                      terms_by_out, out);
+  k_expval_tile_finish<<<(unsigned)((items + 127) / 128), 128, 0, s>>>(partial_acc, nchunks, partial_tile, ntiles,
+                                                                      slots, nterm, terms_by_out, out);
+}
+
+// chunks per state: a function of n only (results do not depend on the batch); 128
+// chunks of 32 tiles at 24 qubits
+int expval_acc_chunks(int n) {
+  const int64_t ntiles = n >= 12 ? (1ll << (n - 12)) : 1;
+  return (int)std::min<int64_t>(ntiles, 128);
+}
+
+void launch_expval_acc(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
+                       const ExpvalTerm* terms, const EvMap* maps, double* partial, int nterm_total, cudaStream_t s) {
+  const size_t amp = c64 ? 8 : 16;
+  const size_t smem = 2 * amp * 4096 + sizeof(double) * kET * (size_t)g.nterm + sizeof(uint64_t) * (4096 >> g.lowq) +
+                      sizeof(uint32_t) * (4096 >> (c64 ? 4 : 3)) + 16 + sizeof(ExpvalTerm) * (size_t)g.nterm +
+                      sizeof(EvMap) * (size_t)g.nmap;
+  static thread_local int set_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (set_dev != dev) {  // the attribute is a ceiling: the device's opt-in maximum, once
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_expval_acc<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncSetAttribute(k_expval_acc<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    set_dev = dev;
+  }
+  const int nchunks = expval_acc_chunks(n);
+  const unsigned grid = (unsigned)(slots * nchunks);
+  if (c64)
+    k_expval_acc<float><<<grid, kET, smem, s>>>((const float2*)states, n, g, terms, maps, partial, nterm_total, nchunks);
+  else
+    k_expval_acc<double><<<grid, kET, smem, s>>>((const double2*)states, n, g, terms, maps, partial, nterm_total,
+                                                 nchunks);
 }
 
 }  // namespace qsb

@@ -41,6 +41,9 @@ struct ExpvalTerm {
   int32_t ny, out;  // #Y, output index
   uint32_t xr;      // register path: X|Y letters in register-bit space of the term's mapping
   uint32_t zsig;    // register path: bit j = parity(tile positions of register j & zl)
+  int32_t path;     // 0: per-thread accumulating kernel (partials [slot][chunk][term]);
+                    // 1: pair-loop kernel (partials [slot][tile][term])
+  int32_t pad;
 };
 // register mapping of a tile group (k = 12): register bit b <-> tile position rpos[b];
 // the terms [term_begin, term_begin + nterm) of the group are evaluated with it
@@ -57,8 +60,14 @@ struct ExpvalGroup {
 void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
                         const ExpvalTerm* terms, const EvMap* maps,
                         double* partial /*[slots][tiles][nterm_total]*/, int nterm_total, cudaStream_t s);
-void launch_expval_tile_finish(const double* partial, int64_t slots, int nterm, int ntiles_log2,
-                               const ExpvalTerm* terms_by_out, double* out, cudaStream_t s);
+void launch_expval_tile_finish(const double* partial_acc, int nchunks, const double* partial_tile, int ntiles,
+                               int64_t slots, int nterm, const ExpvalTerm* terms_by_out, double* out, cudaStream_t s);
+// per-thread accumulating Pauli reducer (k = 12 register mappings, <= kEvAccTerms terms per
+// launch): partials [slot][chunk][nterm_total], chunks = expval_acc_chunks(n)
+constexpr int kEvAccTerms = 32;
+int expval_acc_chunks(int n);
+void launch_expval_acc(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
+                       const ExpvalTerm* terms, const EvMap* maps, double* partial, int nterm_total, cudaStream_t s);
 
 // device-side shot histogram (qsb_hist.cu): sort the per-shot words on their low
 // `nbits` bits and run-length encode -> ascending distinct words + counts
