@@ -721,6 +721,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   std::vector<ExpvalTerm> dev_terms, by_out(nterm);
   std::vector<ExpvalGroup> dev_groups;  // pair-loop launches (path 1)
   std::vector<ExpvalGroup> acc_groups;  // accumulating launches (path 0, k = 12)
+  std::vector<EvClass> dev_classes;
   std::vector<EvMap> dev_maps;
   const int sb = c64 ? 4 : 3;
   for (Grp& g : groups) {
@@ -775,7 +776,26 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
       // launches of <= kEvAccTerms terms (the per-thread accumulators of one launch live
       // in shared memory: kEvAccTerms x 256 doubles)
       auto flush_launch = [&](ExpvalGroup& cur) {
-        if (cur.nterm) acc_groups.push_back(cur);
+        if (cur.nterm) {  // its classes: runs of equal xr per mapping part (Re before Im)
+          cur.cls_begin = (int)dev_classes.size();
+          for (int mi = 0; mi < cur.nmap; ++mi) {
+            const EvMap& m = dev_maps[cur.map_begin + mi];
+            const int tb = m.term_begin - cur.term_begin, te = tb + m.nterm;
+            for (int t = tb; t < te;) {
+              const uint32_t xr = dev_terms[cur.term_begin + t].xr;
+              int e = t, im0 = -1;
+              while (e < te && dev_terms[cur.term_begin + e].xr == xr) {
+                if (im0 < 0 && (dev_terms[cur.term_begin + e].ny & 1)) im0 = e;
+                ++e;
+              }
+              dev_classes.push_back(EvClass{(int16_t)mi, (int16_t)xr, (int16_t)t, (int16_t)(im0 < 0 ? e : im0),
+                                            (int16_t)e, 0});
+              t = e;
+            }
+          }
+          cur.ncls = (int)dev_classes.size() - cur.cls_begin;
+          acc_groups.push_back(cur);
+        }
         cur = ExpvalGroup{};
         cur.smask = g.S;
         cur.k = k;
@@ -860,12 +880,17 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   const size_t pbytes = sizeof(double) * (acc_words + (any_tile ? (size_t)slots * nterm * ((size_t)1 << ntl) : 0));
   QSB_CUDA(ctx->misc.ensure(pbytes + 64));
   QSB_CUDA(ctx->misc2.ensure(sizeof(ExpvalTerm) * 2 * (nterm + 1) + sizeof(double) * nterm * slots +
-                              sizeof(EvMap) * (dev_maps.size() + 1) + 64));
+                              sizeof(EvMap) * (dev_maps.size() + 1) + sizeof(EvClass) * (dev_classes.size() + 1) +
+                              64));
   char* base = ctx->misc2.as<char>();
   ExpvalTerm* d_terms = reinterpret_cast<ExpvalTerm*>(base);
   ExpvalTerm* d_byout = d_terms + (nterm + 1);
   double* d_out = reinterpret_cast<double*>(d_byout + (nterm + 1));
   EvMap* d_maps = reinterpret_cast<EvMap*>(d_out + nterm * slots);
+  EvClass* d_classes = reinterpret_cast<EvClass*>(d_maps + dev_maps.size() + 1);
+  if (!dev_classes.empty())
+    QSB_CUDA(cudaMemcpyAsync(d_classes, dev_classes.data(), sizeof(EvClass) * dev_classes.size(),
+                             cudaMemcpyHostToDevice, ctx->stream));
   if (!dev_maps.empty())
     QSB_CUDA(cudaMemcpyAsync(d_maps, dev_maps.data(), sizeof(EvMap) * dev_maps.size(), cudaMemcpyHostToDevice,
                              ctx->stream));
@@ -877,7 +902,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   double* p_acc = ctx->misc.as<double>();
   double* p_tile = p_acc + acc_words;
   for (const ExpvalGroup& g : acc_groups)
-    launch_expval_acc(c64, amps, n, slots, g, d_terms, d_maps, p_acc, nterm, ctx->stream);
+    launch_expval_acc(c64, amps, n, slots, g, d_terms, d_maps, d_classes, p_acc, nterm, ctx->stream);
   for (const ExpvalGroup& g : dev_groups)
     if (g.nterm)
       launch_expval_tile(c64, amps, n, slots, g, d_terms, d_maps, p_tile, nterm, ctx->stream);

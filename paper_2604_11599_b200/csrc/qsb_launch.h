@@ -55,7 +55,13 @@ struct EvMap {
 struct ExpvalGroup {
   uint64_t smask;   // tile qubits
   int32_t k, lowq, term_begin, nterm;
-  int32_t map_begin, nmap;  // nmap > 0: register-mapped kernel (k == 12)
+  int32_t map_begin, nmap;  // register mappings of the accumulating kernel (k == 12)
+  int32_t cls_begin, ncls;  // its classes (EvClass)
+};
+// a class of the accumulating kernel: a run of terms with equal register X pattern in one
+// mapping (launch-relative indices), Re terms [t0, im0) before Im terms [im0, t1)
+struct EvClass {
+  int16_t map, xr, t0, im0, t1, pad;
 };
 void launch_expval_tile(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
                         const ExpvalTerm* terms, const EvMap* maps,
@@ -64,10 +70,11 @@ void launch_expval_tile_finish(const double* partial_acc, int nchunks, const dou
                                int64_t slots, int nterm, const ExpvalTerm* terms_by_out, double* out, cudaStream_t s);
 // per-thread accumulating Pauli reducer (k = 12 register mappings, <= kEvAccTerms terms per
 // launch): partials [slot][chunk][nterm_total], chunks = expval_acc_chunks(n)
-constexpr int kEvAccTerms = 32;
+constexpr int kEvAccTerms = 16;
 int expval_acc_chunks(int n);
 void launch_expval_acc(int c64, const void* states, int n, int64_t slots, const ExpvalGroup& g,
-                       const ExpvalTerm* terms, const EvMap* maps, double* partial, int nterm_total, cudaStream_t s);
+                       const ExpvalTerm* terms, const EvMap* maps, const EvClass* classes, double* partial,
+                       int nterm_total, cudaStream_t s);
 
 // device-side shot histogram (qsb_hist.cu): sort the per-shot words on their low
 // `nbits` bits and run-length encode -> ascending distinct words + counts
