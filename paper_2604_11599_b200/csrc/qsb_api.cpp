@@ -45,7 +45,7 @@ struct qsb_tape_s {
   qsb_ctx ctx = nullptr;
   TapeInfo info;
   DevBuf d_dev, d_matsrc, d_mats;  // d_mats: literal-only matrix table (no ParamRef angles)
-  std::map<int, std::unique_ptr<PlanDev>> plans;  // key: k * 64 + lowq
+  std::map<std::pair<int, uint64_t>, std::unique_ptr<PlanDev>> plans;  // (geometry, engine options)
   std::unique_ptr<qsb_tape_s> gates_only;          // static sampling view
 };
 
@@ -96,13 +96,14 @@ int get_plan(qsb_tape tp, int c64, int k, int lowq, int rb, PlanDev** out) {
   const bool want_jit = tp->ctx->opt_jit && tp->info.n >= tp->ctx->opt_jit_min;
   const bool fuse = tp->ctx->opt_fuse != 0;
   int key = ((((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0)) * 2 + (fuse ? 1 : 0)) * 2 + c64;
-  auto it = tp->plans.find(key);
+  const std::pair<int, uint64_t> pkey(key, tp->ctx->eopt.key());
+  auto it = tp->plans.find(pkey);
   if (it != tp->plans.end()) {
     *out = it->second.get();
     return QSB_OK;
   }
   auto pd = std::make_unique<PlanDev>();
-  std::string e = build_stream_plan(tp->info, k, lowq, rb, swizzle_bits(c64), pd->plan);
+  std::string e = build_stream_plan(tp->info, k, lowq, rb, swizzle_bits(c64), pd->plan, tp->ctx->eopt);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   StreamPlan& P = pd->plan;
   QSB_CUDA(pd->gates.ensure(std::max<size_t>(1, P.gates.size()) * sizeof(PassGate)));
@@ -143,7 +144,7 @@ int get_plan(qsb_tape tp, int c64, int k, int lowq, int rb, PlanDev** out) {
       fprintf(stderr, "\n");
     }
   *out = pd.get();
-  tp->plans[key] = std::move(pd);
+  tp->plans[pkey] = std::move(pd);
   return QSB_OK;
 }
 
@@ -277,6 +278,14 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   int32_t* d_active = d_copy_src + r.slots;
   int32_t* d_nactive = d_active + r.slots;
   double* d_phys = reinterpret_cast<double*>(ctx->counters.as<char>() + 16);  // [bytes, flops] physical
+  if (dedup) {  // outcome-history rows: one bit per draw (measure / reset ops bound the draws)
+    int ndraw_ops = 0;
+    for (const DevOp& d : t.dev) ndraw_ops += (d.kind == QSB_OP_MEASURE || d.kind == QSB_OP_RESET) ? 1 : 0;
+    a.hwords = std::max(1, (ndraw_ops + 63) / 64);
+    QSB_CUDA(ctx->histbits.ensure(sizeof(uint64_t) * a.hwords * r.slots));
+    QSB_CUDA(cudaMemsetAsync(ctx->histbits.p, 0, sizeof(uint64_t) * a.hwords * r.slots, ctx->stream));
+    a.hbits = ctx->histbits.as<uint64_t>();
+  }
   launch_ctl_init(a.ctl, a.bits, t.nwords, a.guards, t.gwords, r.slots, r.seed, r.shot_begin, r.rng_init, dedup ? 1 : 0,
                   ctx->stream);
   r.launches++;
@@ -451,7 +460,7 @@ int32_t qsb_ctx_destroy(qsb_ctx ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DevBuf* b : {&ctx->state, &ctx->partial, &ctx->ctl, &ctx->bits, &ctx->guards, &ctx->mats, &ctx->params,
                     &ctx->predrawn, &ctx->status, &ctx->counters, &ctx->misc, &ctx->misc2, &ctx->trace,
-                    &ctx->dedup})
+                    &ctx->dedup, &ctx->histbits, &ctx->shotwords, &ctx->histo})
     b->release();
   for (auto e : ctx->pass_events) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_a);
@@ -477,7 +486,7 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
-  else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)      // register-phase gate fusion in the NVRTC kernels    // branch-history deduplication of trajectories
+  else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
     ctx->opt_reg_bits = value;
@@ -486,9 +495,10 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->state, &ctx->partial, &ctx->ctl, &ctx->bits, &ctx->guards, &ctx->mats, &ctx->params,
-                      &ctx->predrawn, &ctx->status, &ctx->misc, &ctx->misc2, &ctx->trace, &ctx->dedup})
+                      &ctx->predrawn, &ctx->status, &ctx->misc, &ctx->misc2, &ctx->trace, &ctx->dedup,
+                      &ctx->histbits})
       b->release();
-  } else return fail(QSB_ERR_ARG, "unknown option " + k);
+  } else if (!ctx->eopt.set(k, value)) return fail(QSB_ERR_ARG, "unknown option " + k);
   return QSB_OK;
 }
 
@@ -1409,8 +1419,7 @@ int sample_static_impl(qsb_tape tp, int32_t precision, const double* params, uin
     mq.push_back(t.dev[idx].qubit);
     mb.push_back(t.dev[idx].bit);
   }
-  size_t N = (size_t)1 << t.n;
-  cudaError_t e = ctx->misc.ensure(sizeof(double) * N + 64);
+  cudaError_t e = ctx->misc.ensure(sizeof(double) * (size_t)cdf_blocks(t.n) + 64);
   if (e == cudaSuccess) e = ctx->misc2.ensure(sizeof(int32_t) * 2 * (mq.size() + 1) + sizeof(uint64_t) * t.nwords * shot_count);
   if (e != cudaSuccess) {
     qsb_state_destroy(st);
@@ -1425,8 +1434,8 @@ int sample_static_impl(qsb_tape tp, int32_t precision, const double* params, uin
     QSB_CUDA(cudaMemcpyAsync(d_mb, mb.data(), sizeof(int32_t) * mb.size(), cudaMemcpyHostToDevice, ctx->stream));
   }
   launch_cumsum_seq(st->c64, st->amps.p, t.n, ctx->misc.as<double>(), ctx->stream);
-  launch_static_search(ctx->misc.as<double>(), t.n, seed, shot_begin, shot_count, d_mq, d_mb, (int)mq.size(), t.nwords,
-                       dev_out ? dev_out : d_bits, ctx->stream);
+  launch_static_search(st->c64, st->amps.p, ctx->misc.as<double>(), t.n, seed, shot_begin, shot_count, d_mq, d_mb,
+                       (int)mq.size(), t.nwords, dev_out ? dev_out : d_bits, ctx->stream);
   e = cudaSuccess;
   if (!dev_out)
     e = cudaMemcpyAsync(bits_out, d_bits, sizeof(uint64_t) * t.nwords * shot_count, cudaMemcpyDeviceToHost, ctx->stream);

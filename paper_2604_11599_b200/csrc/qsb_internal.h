@@ -220,6 +220,11 @@ struct StreamArgs {
   // active[0 .. *nactive) (null: every slot)
   const int32_t* active;
   const int32_t* nactive;
+  // ... whose keys are verified on the exact outcome history: bit d of slot s's row is
+  // the outcome of its d-th draw (null: no dedup)
+  uint64_t* hbits;
+  int32_t hwords;
+  int32_t pad_h;
 };
 
 QSB_HD uint64_t insert_zero(uint64_t v, int pos) {

@@ -20,6 +20,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 #include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -92,10 +93,22 @@ uint64_t fnv1a(const std::string& s) {
   return h;
 }
 
+// cubin cache: $QSB_JIT_CACHE, else a per-user directory ($XDG_CACHE_HOME or ~/.cache, then
+// /tmp/qsb_jit_cache-<uid>) created 0700 -- never a shared, predictable world-writable path
 std::string cache_dir() {
   const char* e = getenv("QSB_JIT_CACHE");
-  std::string d = e && *e ? e : "/tmp/qsb_jit_cache";
-  mkdir(d.c_str(), 0755);
+  std::string d;
+  if (e && *e) {
+    d = e;
+  } else if (const char* x = getenv("XDG_CACHE_HOME"); x && *x) {
+    d = std::string(x) + "/qsb_jit";
+  } else if (const char* h = getenv("HOME"); h && *h) {
+    mkdir((std::string(h) + "/.cache").c_str(), 0700);
+    d = std::string(h) + "/.cache/qsb_jit";
+  } else {
+    d = "/tmp/qsb_jit_cache-" + std::to_string((unsigned)getuid());
+  }
+  mkdir(d.c_str(), 0700);
   return d;
 }
 
@@ -274,11 +287,7 @@ std::string sparse_helper(uint32_t z) {
 // coefficient part instead of two FFMA -- (mr, mr) * (xr, xi) and (-mi, mi) * (xi, xr), the
 // swapped operand being a free LO_HI operand modifier.  Halves the FP32 instructions of a
 // block (complex64 passes are issue / instruction-fetch bound).  $QSB_JIT_FFMA2=0 disables.
-bool packed_blocks(int c64) {
-  const char* e = getenv("QSB_JIT_FFMA2");
-  if (e && *e) return c64 && atoi(e) == 1;
-  return c64 != 0;
-}
+bool packed_blocks(const StreamPlan& P, int c64) { return c64 && P.opt.ffma2 == 1; }
 
 void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr, bool packed) {
   const int d = f.qb < 0 ? 2 : 4;
@@ -334,21 +343,16 @@ void emit_block(std::ostringstream& o, const FuseItem& f, int cf, int nr, bool p
   o << "  }\n";
 }
 
-bool edge_x_disabled() {
-  const char* e = getenv("QSB_JIT_EDGE_X");
-  return e && *e && atoi(e) == 0;
-}
+bool edge_x_disabled(const StreamPlan& P) { return P.opt.edge_x == 0; }
 
 // Phases are separate __noinline__ functions (ptxas time linear in the phases) except for
 // complex128, where inlining them into the pass kernel measured 2.2 % faster on B200 (DYN20
 // pass time 607.8 -> 594.5 ms per 2048 shots; no callee-saved spills at phase boundaries)
 // for ~1.7x the NVRTC time; complex64 measured 7 % slower inlined.  $QSB_JIT_INLINE_PHASES
 // = 0 / 1 overrides.
-bool inline_phases(int c64, int pass_gates) {
-  const char* e = getenv("QSB_JIT_INLINE_PHASES");
-  if (e && *e) return atoi(e) == 1;
-  const char* mg = getenv("QSB_JIT_INLINE_MIN_GATES");
-  return !c64 && pass_gates >= (mg && *mg ? atoi(mg) : 0);
+bool inline_phases(const StreamPlan& P, int c64, int pass_gates) {
+  if (P.opt.inline_phases >= 0) return P.opt.inline_phases == 1;
+  return !c64 && pass_gates >= P.opt.inline_min_gates;
 }
 
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
@@ -360,7 +364,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
       << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
          "const int tid, A* __restrict__ dst, const uint64_t* __restrict__ hi_off, MID mid) {\n";
   } else {
-    o << (inline_phases(c64, pd.pgate_count) ? "__device__ __forceinline__ void ph" : "__device__ __noinline__ void ph") << ph_index
+    o << (inline_phases(P, c64, pd.pgate_count) ? "__device__ __forceinline__ void ph" : "__device__ __noinline__ void ph") << ph_index
       << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
          "const int tid) {\n";
   }
@@ -372,7 +376,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
   // slot base at the phase's loads / stores (the slot map is XOR-linear in the register
   // index) instead of a branch whose join needs 2 x 16 register moves
   std::vector<int> edge(items.size(), 0);  // 1: at the loads, 2: at the stores
-  if (!edge_x_disabled()) {
+  if (!edge_x_disabled(P)) {
     auto bits_of = [&](const FuseItem& it) -> uint32_t {
       if (it.gate < 0) return (1u << it.qa) | (it.qb >= 0 ? 1u << it.qb : 0u);
       const PhaseGate& q = P.phase_gates[it.gate];
@@ -421,7 +425,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
     const FuseItem& item = items[ii];
     if (edge[ii]) continue;
     if (item.gate < 0) {
-      emit_block(o, item, cf, nr, packed_blocks(c64));
+      emit_block(o, item, cf, nr, packed_blocks(P, c64));
       cf += item.qb < 0 ? 8 : 32;
       continue;
     }
@@ -555,16 +559,11 @@ bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass) {
   return false;
 }
 
-// buffering mode of a pass kernel (qsb_pass_common.cuh).  MODE 1 (two thread groups over
-// a three-tile ring, complex128) is opt-in ($QSB_PASS_MODE=1): measured on B200 it is
-// 6-20 % slower than MODE 0 (the per-item context loads and the mbarrier waits sit on
-// each group's critical path; ncu: long_scoreboard 18-27 % vs 6-12 %).
-int jit_pass_mode(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
-  const char* e = getenv("QSB_PASS_MODE");
-  if (c64 || !(e && *e && atoi(e) == 1)) return 0;
-  const size_t sm = pass_reg_smem(c64, P.passes[pass], P.rb, t.n, pass_needs_stage(t, P, pass), 1);
-  return sm <= 227 * 1024 ? 1 : 0;
-}
+// buffering mode of a pass kernel (qsb_pass_common.cuh): one thread group per CTA, two
+// CTAs per SM.  (Round 1 also shipped a two-group / three-tile-ring mode, measured 6-20 %
+// slower on B200 -- the per-item context loads and mbarrier waits sat on each group's
+// critical path -- and it was removed.)
+int jit_pass_mode(const TapeInfo&, const StreamPlan&, int, int) { return 0; }
 
 // DIRECT last phase (qsb_pass_common.cuh): complex128 MODE 0 passes without an epilogue
 // and without per-item gate staging whose last phase is a register phase with coalesced
@@ -573,8 +572,7 @@ int jit_pass_mode(const TapeInfo& t, const StreamPlan& P, int pass, int c64) {
 // stores uncoalesced); staged passes (ParamRef, VQE24) measured slower, so they are
 // excluded.  $QSB_LAST_DIRECT=0 disables, =2 also allows staged passes.
 bool jit_pass_direct(const TapeInfo& t, const StreamPlan& P, int pass, int c64, int mode) {
-  const char* e = getenv("QSB_LAST_DIRECT");
-  const int lvl = e && *e ? atoi(e) : 1;
+  const int lvl = P.opt.last_direct;
   if (lvl == 0) return false;
   const PassDesc& pd = P.passes[pass];
   if (c64 || mode != 0 || pd.epi || pd.phase_count < 1) return false;
@@ -585,8 +583,7 @@ bool jit_pass_direct(const TapeInfo& t, const StreamPlan& P, int pass, int c64, 
   // 2^s consecutive amplitudes), lanes advance by 2^s amplitudes and a warp store covers
   // 16-byte pieces of 2^s * 16-byte runs that the thread's other registers complete
   // (merged in L2).  s <= $QSB_LAST_DIRECT_MAXLOW (default 0: lanes 0..7 cover 128 B).
-  const char* ml = getenv("QSB_LAST_DIRECT_MAXLOW");
-  const int maxlow = ml && *ml ? atoi(ml) : 0;
+  const int maxlow = P.opt.last_direct_maxlow;
   uint32_t tmask = 0;
   for (int i = 0; i < ph.nt; ++i) tmask |= 1u << ph.tpos[i];
   int s = 0;
@@ -615,9 +612,8 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   // packed f32x2 arithmetic pays in the fused complex64 blocks (-6 % DYN20 pass time); the
   // packed versions of the single-gate helpers (kPackedHelpers, bit-identical) measured no
   // gain on DYN20 and a loss on RDC30 / VQE24 ($QSB_JIT_PACKED_GATES=1 selects them)
-  const bool packed = packed_blocks(c64);
-  const char* pg = getenv("QSB_JIT_PACKED_GATES");
-  const bool packed_gates = packed && pg && *pg && atoi(pg) == 1;
+  const bool packed = packed_blocks(P, c64);
+  const bool packed_gates = packed && P.opt.packed_gates == 1;
   o << (packed_gates ? kPackedHelpers : kHelpers);
   if (packed && !packed_gates)
     o << "__device__ __forceinline__ A ffma2(A a, A b, A c) {\n  unsigned long long d;\n"
@@ -651,7 +647,7 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
     if (!pd.pgate_count) o << "0";
     o << "};\n";
   }
-  if (!cfv.empty() && packed_blocks(c64)) {  // (mr, mr), (-mi, mi) per complex entry, same indices
+  if (!cfv.empty() && packed_blocks(P, c64)) {  // (mr, mr), (-mi, mi) per complex entry, same indices
     o << "__constant__ float2 qsb_cf2[" << cfv.size() << "] = {";
     for (size_t i = 0; i + 1 < cfv.size(); i += 2) {
       char buf[160];
@@ -683,9 +679,8 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   if (direct)
     o << "struct LastPhase {\n  template <typename MID> __device__ void operator()(const qsb::PassCtx<R>& cx, A* dst, "
          "const uint64_t* hi_off, MID mid) const {\n    phL(cx.tile, cx.swz, cx.sg, cx.tid, dst, hi_off, mid);\n  }\n};\n";
-  const char* mb = getenv("QSB_JIT_MINBLOCKS");  // tuning knob: CTAs per SM the register budget targets
-  o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
-    << (mode == 1 ? 1 : (mb && *mb ? atoi(mb) : 2)) << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << std::max(1, P.opt.minblocks)
+    << ") qsb_jit_pass(qsb::StreamArgs a, qsb::PassDesc pd) {\n";
   o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
   o << "  qsb::pass_persistent<R, " << P.rb << ", " << (stage ? "true" : "false") << ", " << mode << ", "
     << (direct ? "true" : "false") << ">(a, pd, smem_raw, [&](const qsb::PassCtx<R>& cx) {\n";
@@ -699,6 +694,19 @@ std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64
   else o << "  });\n}\n";
   return o.str();
 }
+
+namespace {
+// write-then-rename with a name unique per process and thread: concurrent ranks compiling
+// the same pass never expose a partially written file under the final name
+void write_cache(const std::string& path, const std::vector<char>& cubin) {
+  const std::string tmp = path + ".tmp." + std::to_string((long)getpid()) + "." +
+                          std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
+  std::ofstream f(tmp, std::ios::binary);
+  f.write(cubin.data(), (std::streamsize)cubin.size());
+  f.close();
+  if (!f || rename(tmp.c_str(), path.c_str()) != 0) unlink(tmp.c_str());
+}
+}  // namespace
 
 std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, std::vector<JitKernel>& out,
                       double* compile_ms, int* compiled, int* cached) {
@@ -743,13 +751,7 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
         Job& j = jobs[i];
         if (j.ok) continue;
         j.ok = compile_one(j.src, j.cubin, j.log);
-        if (j.ok) {
-          std::string tmp = j.path + ".tmp" + std::to_string(i);
-          std::ofstream f(tmp, std::ios::binary);
-          f.write(j.cubin.data(), (std::streamsize)j.cubin.size());
-          f.close();
-          rename(tmp.c_str(), j.path.c_str());
-        }
+        if (j.ok) write_cache(j.path, j.cubin);
       }
     });
   for (auto& th : pool) th.join();
@@ -760,6 +762,18 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
     }
     cudaLibrary_t lib;
     cudaError_t e = cudaLibraryLoadData(&lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess && j.from_cache) {  // a damaged cache entry: drop it, compile afresh
+      cudaGetLastError();
+      unlink(j.path.c_str());
+      j.from_cache = false;
+      j.ok = compile_one(j.src, j.cubin, j.log);
+      if (!j.ok) {
+        jit_release(out);
+        return "NVRTC failed for pass " + std::to_string(j.pass) + ": " + j.log.substr(0, 2000);
+      }
+      write_cache(j.path, j.cubin);
+      e = cudaLibraryLoadData(&lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    }
     if (e != cudaSuccess) {
       jit_release(out);
       return std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
@@ -784,10 +798,9 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
     }
     int per_sm = 1, dev = 0, sms = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k, jk.threads, jk.smem);
-    // $QSB_JIT_CTAS_PER_SM caps the persistent grid (experiment: two contexts on two
+    // option ctas_per_sm caps the persistent grid (experiment: two contexts on two
     // streams sharing the SMs, experiments/two_stream.py)
-    if (const char* e = getenv("QSB_JIT_CTAS_PER_SM"))
-      if (atoi(e) > 0) per_sm = std::min(per_sm, atoi(e));
+    if (P.opt.ctas_per_sm > 0) per_sm = std::min(per_sm, P.opt.ctas_per_sm);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     jk.max_grid = (int64_t)std::max(1, per_sm) * sms;

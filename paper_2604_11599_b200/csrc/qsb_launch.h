@@ -83,9 +83,13 @@ cudaError_t launch_histogram(const uint64_t* words, uint64_t* sorted, size_t n, 
                              int32_t* counts, int32_t* nruns, void* scratch, size_t scratch_bytes, cudaStream_t s);
 
 // static sampling
-void launch_cumsum_seq(int c64, const void* amps, int n, double* cdf, cudaStream_t s);
-void launch_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
-                          const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits,
+// static sampling (sim.py:354-369), bit-exact: one sequential pass keeps the running sum
+// at the end of every block (cdf_blocks(n) doubles); each shot searches the blocks and
+// re-runs its block's left-to-right additions
+int64_t cdf_blocks(int n);
+void launch_cumsum_seq(int c64, const void* amps, int n, double* ends, cudaStream_t s);
+void launch_static_search(int c64, const void* amps, const double* ends, int n, uint64_t seed, int64_t shot_begin,
+                          int64_t count, const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits,
                           cudaStream_t s);
 
 // ---- resident engine (qsb_resident.cu) -------------------------------------

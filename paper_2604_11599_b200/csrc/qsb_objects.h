@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/qsb.h"
+#include "qsb_plan.h"
 
 namespace qsb {
 // record `msg` as qsb_last_error() and return `code`
@@ -67,8 +68,10 @@ struct qsb_ctx_s {
   std::vector<cudaEvent_t> pass_events;
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
   int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1, opt_lowq = 0;
+  qsb::EngineOptions eopt;  // planner / NVRTC generator options (qsb_plan.h)
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
   DevBuf shotwords, histo;  // device-side shot histogram (qsb_sample_counts)
+  DevBuf histbits;          // exact outcome histories of the dedup'd batch
   qsb_stats last{};
   double run_flops = 0;  // floating-point work of the pass kernels in the current run
   bool run_physical = false;  // dedup ran: bytes / flops come from the device counters

@@ -177,19 +177,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       : "memory");
 }
 
-// Buffering modes of the persistent driver.
-//   MODE 0: each CTA (2 per SM) walks its items alone: complex64 tiles (32 KiB)
-//           double-buffer; complex128 tiles (64 KiB) keep one buffer, whose scatter
-//           overlaps the next gather, and the two CTAs of an SM overlap each other.
-//   MODE 1 (complex128, NVRTC kernels): one CTA per SM with two thread groups and a
-//           ring of three tile buffers.  Local item i runs on group i % 2 in buffer
-//           i % 3; when a group has taken item i into registers it issues the gather of
-//           item i + 3 into the same buffer (consumed by the other group), so every
-//           gather is in flight while both groups compute.  Completion is signalled
-//           through mbarriers (cp.async.mbarrier.arrive) indexed i % 6, which keeps
-//           the parity of a wait unambiguous (item i - 6 ran on the same group).
-__host__ __device__ inline int pass_buffers(int c64, int mode) { return mode == 1 ? 3 : (c64 ? 2 : 1); }
-__host__ __device__ inline int pass_groups(int mode) { return mode == 1 ? 2 : 1; }
+// Buffering of the persistent driver: each CTA (2 per SM) walks its items alone;
+// complex64 tiles (32 KiB) double-buffer, complex128 tiles (64 KiB) keep one buffer whose
+// scatter overlaps the next gather, and the two CTAs of an SM overlap each other.  (A
+// two-group / three-tile-ring mode with mbarrier hand-off was measured 6-20 % slower in
+// round 1 and removed; `mode` stays in the signatures as 0.)
+__host__ __device__ inline int pass_buffers(int c64, int mode) { return c64 ? 2 : 1; }
+__host__ __device__ inline int pass_groups(int mode) { return 1; }
 
 // dynamic shared memory of a register-blocked pass
 __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int rb, int n, bool stage, int mode = 0) {
@@ -199,8 +193,7 @@ __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int
   const int G = pass_groups(mode);
   return pass_buffers(c64, mode) * (amp << pd.k) + G * (stage ? sgate * pd.pgate_count : 0) +
          (sizeof(uint64_t) << (pd.k - pd.lowq)) + (sizeof(uint32_t) << (pd.k - sb)) +
-         G * sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) + item_tables_bytes(n) + 16 +
-         (mode == 1 ? 6 * (sizeof(uint64_t) + sizeof(PassItem)) + 16 : 0);
+         G * sizeof(double) * (1u << (pd.k - rb)) + sizeof(uint32_t) * (1u << rb) + item_tables_bytes(n) + 16;
 }
 
 
@@ -223,15 +216,16 @@ template <typename R, int RB, bool STAGE = true, int MODE = 0, bool DIRECT = fal
           typename LastRunner = NoLastPhase>
 __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassDesc& pd, unsigned char* smem_raw,
                                                 PhaseRunner run, LastRunner run_last = LastRunner()) {
+  static_assert(MODE == 0, "single-group driver");
   using A = typename Amp<R>::T;
   constexpr int SB = sizeof(R) == 8 ? 3 : 4;
-  constexpr int G = MODE == 1 ? 2 : 1;  // thread groups
-  constexpr int NB = MODE == 1 ? 3 : (sizeof(R) == 4 ? 2 : 1);  // pass_buffers()
+  constexpr int G = 1;                             // thread groups
+  constexpr int NB = sizeof(R) == 4 ? 2 : 1;       // pass_buffers()
   const int k = pd.k, TL = 1 << k, T = TL >> RB;
-  const int grp = MODE == 1 ? (int)(threadIdx.x >= (unsigned)T) : 0;
-  const int tid = (int)threadIdx.x - grp * T;  // thread index inside the group
-  const int ctid = threadIdx.x, CT = G * T;    // whole CTA (table set-up)
-  const int bar = MODE == 1 ? 1 + grp : 0;
+  const int grp = 0;
+  const int tid = (int)threadIdx.x;
+  const int ctid = threadIdx.x, CT = G * T;        // whole CTA (table set-up)
+  const int bar = 0;
   A* bufs = reinterpret_cast<A*>(smem_raw);
   SGate<R>* sg0 = reinterpret_cast<SGate<R>*>(bufs + NB * TL);
   SGate<R>* sg = sg0 + (STAGE ? grp * pd.pgate_count : 0);
@@ -244,8 +238,6 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   itb.pdt = reinterpret_cast<uint64_t*>((reinterpret_cast<size_t>(ujt + (1 << RB)) + 15) & ~(size_t)15);
   itb.pxo = itb.pdt + item_chunks(a.n) * 16;
   itb.pxs = reinterpret_cast<uint32_t*>(itb.pxo + item_chunks(a.n) * 16);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(((reinterpret_cast<size_t>(itb.pxs + item_chunks(a.n) * 16)) + 7) &
-                                               ~(size_t)7);
   build_item_tables(itb, pd, a.n, ctid, CT);
   const uint64_t lowm = (1ull << pd.lowq) - 1;
   const uint64_t shi = pd.smask & ~lowm;
@@ -257,9 +249,6 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
       if (hh & 1) s ^= V[p];
     swz[h] = s;
   }
-  PassItem* ctxs = reinterpret_cast<PassItem*>(mbar + 6);  // MODE 1: item contexts, by local item % 6
-  if (MODE == 1 && ctid < 6) mbar_init(&mbar[ctid], T + 1);
-  if (MODE == 1) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
   // Tile element l = tid + j*T (j < 2^RB; tid and j*T occupy disjoint bits, and
   // T is a multiple of 2^lowq and of 2^SB).  pdep and the swizzle are both linear
@@ -429,57 +418,6 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
 #pragma unroll
     for (int j = 0; j < (1 << RB); ++j) st[pb | hi_off[j * hstep]] = v[j];
   };
-
-  if (MODE == 1) {
-    // a contiguous range of items per CTA: consecutive items are tiles of the same state,
-    // so the loader re-reads a TrajCtl only when the state changes (the context is then
-    // off the groups' critical path)
-    const int64_t per = (W + gridDim.x - 1) / gridDim.x;
-    const int64_t wbeg = (int64_t)blockIdx.x * per;
-    const int64_t nloc = W > wbeg ? (W - wbeg < per ? W - wbeg : per) : 0;
-    auto wof = [&](int64_t i) { return wbeg + i; };
-    SlotCtx sc;
-    sc.idx = -1;
-    auto ctx_of = [&](int64_t i) {
-      const int64_t w = wof(i);
-      if ((w >> ntl) != sc.idx) sc = slot_ctx(a, pd, w >> ntl);
-      return item_of(sc, pd, (uint64_t)w & ((1ull << ntl) - 1), ntl, a.n, itb);
-    };
-    // gather of local item i (context it) into buffer i % 3 by the calling group; every
-    // thread arrives on mbar[i % 6] when its copies have landed, thread 0 once more
-    // after publishing the context in ctxs[i % 6]
-    auto load = [&](int64_t i, const PassItem& it) {
-      uint64_t* mb = &mbar[i % 6];
-      prefetch(it, bufs + (i % 3) * TL);
-      if (it.alive && !pd.init_zero) mbar_arrive_cp_async(mb);
-      else mbar_arrive(mb);
-      if (tid == 0) {
-        ctxs[i % 6] = it;
-        mbar_arrive(mb);
-      }
-    };
-    if (grp == 0) {
-      if (nloc > 0) load(0, ctx_of(0));
-      if (nloc > 2) load(2, ctx_of(2));
-    } else if (nloc > 1) {
-      load(1, ctx_of(1));
-    }
-    for (int64_t i = grp; i < nloc; i += 2) {
-      const bool more = i + 3 < nloc;
-      // one warp polls the mbarrier; the rest of the group sleeps in the named barrier
-      // instead of spinning on try_wait (which steals issue slots from the other group)
-      if (tid < 32) mbar_wait(&mbar[i % 6], (uint32_t)((i / 6) & 1));
-      group_sync(bar, T);
-      const PassItem it = ctxs[i % 6];
-      A v[1 << RB];
-      if (it.alive) process(it, bufs + (i % 3) * TL, v);
-      group_sync(bar, T);  // the group is done with the buffer
-      if (more) load(i + 3, ctx_of(i + 3));
-      if (it.alive) scatter(it, v);
-    }
-    cp_async_wait0();
-    return;
-  }
 
   int64_t w = blockIdx.x;
   PassItem cur;

@@ -243,10 +243,10 @@ struct Planner {
   const TapeInfo& t;
   int k, lowq, rb;
   int swz_bits_ = 3;
-  bool pair_aware_ = getenv("QSB_PAIR_AWARE") ? atoi(getenv("QSB_PAIR_AWARE")) != 0 : true;
-  bool phase_search_ = getenv("QSB_PHASE_SEARCH") ? atoi(getenv("QSB_PHASE_SEARCH")) != 0 : false;
-  bool block_condx_ = getenv("QSB_BLOCK_CONDX") ? atoi(getenv("QSB_BLOCK_CONDX")) != 0 : false;
   StreamPlan& P;
+  bool pair_aware_ = P.opt.pair_aware != 0;
+  bool phase_search_ = P.opt.phase_search != 0;
+  bool block_condx_ = P.opt.block_condx != 0;
   std::vector<RegionBuild> regions;
 
   Planner(const TapeInfo& t_, int k_, int lowq_, int rb_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), rb(rb_), P(p) {}
@@ -696,8 +696,28 @@ struct Planner {
 
 }  // namespace
 
-std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz, StreamPlan& out) {
+bool EngineOptions::set(const std::string& key, int64_t value) {
+  const int v = (int)value;
+  if (key == "pair_aware") pair_aware = v;
+  else if (key == "phase_search") phase_search = v;
+  else if (key == "block_condx") block_condx = v;
+  else if (key == "inline_phases") inline_phases = v;
+  else if (key == "inline_min_gates") inline_min_gates = v;
+  else if (key == "ffma2") ffma2 = v;
+  else if (key == "packed_gates") packed_gates = v;
+  else if (key == "last_direct") last_direct = v;
+  else if (key == "last_direct_maxlow") last_direct_maxlow = v;
+  else if (key == "minblocks") minblocks = v;
+  else if (key == "edge_x") edge_x = v;
+  else if (key == "ctas_per_sm") ctas_per_sm = v;
+  else return false;
+  return true;
+}
+
+std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz, StreamPlan& out,
+                              const EngineOptions& opt) {
   out = StreamPlan();
+  out.opt = opt;
   k = std::max(1, std::min(k, std::min(t.n, kMaxTile)));
   lowq = std::max(0, std::min(lowq, k));
   out.k = k;

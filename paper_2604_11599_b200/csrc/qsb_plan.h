@@ -36,7 +36,35 @@ uint32_t swizzle_hi(uint32_t hi, int sb);  // V applied to tile bits >= sb (hi =
 // offset of each of the 2^rb registers
 void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff);
 
+// Engine options of the planner and the NVRTC generator, set per context
+// (qsb_ctx_set_option); the defaults are the settings measured best on B200 (DESIGN.md
+// §7b).  Part of the plan cache key.
+struct EngineOptions {
+  int pair_aware = 1;         // phase register sets follow two-qubit partners
+  int phase_search = 0;       // per-phase register-set search
+  int block_condx = 0;        // a conditional X ends its target's use in a phase
+  int inline_phases = -1;     // phases inlined into the pass kernel (-1: complex128 yes, complex64 no)
+  int inline_min_gates = 0;   // ... only for passes with at least this many gates
+  int ffma2 = 1;              // complex64 fused blocks as packed fma.rn.f32x2
+  int packed_gates = 0;       // complex64 single-gate helpers packed too (bit-identical)
+  int last_direct = 1;        // last phase stores to HBM: 0 off, 1 unstaged passes, 2 also staged
+  int last_direct_maxlow = 0; // ... with at most this many low tile positions in registers
+  int minblocks = 2;          // CTAs per SM the register budget of a pass kernel targets
+  int edge_x = 1;             // conditional X gates at a phase edge as slot-base XORs
+  int ctas_per_sm = 0;        // cap of the persistent pass grid per SM (0: occupancy)
+  uint64_t key() const {
+    const int v[] = {pair_aware, phase_search, block_condx, inline_phases, inline_min_gates, ffma2, packed_gates,
+                     last_direct, last_direct_maxlow, minblocks, edge_x, ctas_per_sm};
+    uint64_t h = 1469598103934665603ull;
+    for (int x : v) h = (h ^ (uint64_t)(uint32_t)x) * 1099511628211ull;
+    return h;
+  }
+  // set a named option; false if `key` is not an engine option
+  bool set(const std::string& key, int64_t value);
+};
+
 struct StreamPlan {
+  EngineOptions opt;  // the options the plan (and its NVRTC kernels) were built with
   int k = 0, lowq = 0, ntiles_log2 = 0, rb = 0;
   std::vector<PassDesc> passes;
   std::vector<PassGate> gates;
@@ -63,7 +91,8 @@ double pass_flops(const TapeInfo& t, const StreamPlan& P, int pass);
 
 // rb = register bits of k_pass_reg (4 for complex128, 5 for complex64); phases are
 // built when k - rb >= 5 (at least one warp per tile), else the shared-memory kernel runs.
-std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz_bits, StreamPlan& out);
+std::string build_stream_plan(const TapeInfo& t, int k, int lowq, int rb, int swz_bits, StreamPlan& out,
+                              const EngineOptions& opt = EngineOptions());
 
 }  // namespace qsb
 

@@ -191,29 +191,53 @@ __global__ void k_expval_finish(const double* partial, int64_t slots, int nterm,
 }
 
 // ---- static sampling (sim.py:354-369) ---------------------------------------------
-template <typename R> __global__ void k_cumsum_seq(const typename Amp<R>::T* amps, int64_t N, double* cdf) {
-  // numpy.cumsum is a strict left-to-right sum; reproduce it exactly with one thread.
+// numpy.cumsum is a strict left-to-right sum whose every partial is rounded; it is
+// reproduced bit-exactly without a 2^n CDF buffer: ONE sequential pass (one thread, the
+// only order that yields those roundings) keeps just the running value at the end of
+// every block of kCdfBlock amplitudes; each shot then finds its block by a binary search
+// over those values and re-runs the same left-to-right additions inside that block from
+// the block's exact starting value.  Memory: 2^n / kCdfBlock doubles.
+constexpr int kCdfBlock = 1024;
+
+template <typename R> __global__ void k_cumsum_blocks(const typename Amp<R>::T* amps, int64_t N, double* ends) {
   double c = 0.0;
-  for (int64_t i = 0; i < N; ++i) {
-    c = __dadd_rn(c, norm2<R>(amps[i]));
-    cdf[i] = c;
+  for (int64_t b = 0; b < N; b += kCdfBlock) {
+    const int64_t e = b + kCdfBlock < N ? b + kCdfBlock : N;
+#pragma unroll 8
+    for (int64_t i = b; i < e; ++i) c = __dadd_rn(c, norm2<R>(amps[i]));
+    ends[b / kCdfBlock] = c;
   }
 }
 
-__global__ void k_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
-                                const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits) {
+template <typename R>
+__global__ void k_static_search(const typename Amp<R>::T* amps, const double* ends, int n, uint64_t seed,
+                                int64_t shot_begin, int64_t count, const int32_t* mq, const int32_t* mb, int nmeas,
+                                int nwords, uint64_t* bits) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= count) return;
   uint64_t rs[4];
   rng_for_shot(rs, seed, (uint64_t)(shot_begin + s));
   double u = rng_uniform(rs);
-  int64_t N = 1ll << n, lo = 0, hi = N;
-  while (lo < hi) {  // searchsorted(side="right"): first index with cdf > u
+  const int64_t N = 1ll << n, nb = (N + kCdfBlock - 1) / kCdfBlock;
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {  // first block whose last partial sum is > u
     int64_t mid = (lo + hi) >> 1;
-    if (cdf[mid] <= u) lo = mid + 1;
+    if (ends[mid] <= u) lo = mid + 1;
     else hi = mid;
   }
-  int64_t idx = lo < N - 1 ? lo : N - 1;
+  int64_t idx = N;  // searchsorted(side="right"): first index with cum > u (N if none)
+  if (lo < nb) {
+    double c = lo ? ends[lo - 1] : 0.0;
+    const int64_t b0 = lo * kCdfBlock, e = b0 + kCdfBlock < N ? b0 + kCdfBlock : N;
+    for (int64_t i = b0; i < e; ++i) {
+      c = __dadd_rn(c, norm2<R>(amps[i]));
+      if (c > u) {
+        idx = i;
+        break;
+      }
+    }
+  }
+  idx = idx < N - 1 ? idx : N - 1;
   uint64_t* b = bits + s * nwords;
   for (int w = 0; w < nwords; ++w) b[w] = 0;
   for (int j = 0; j < nmeas; ++j) {  // later writes to the same bit win
@@ -304,16 +328,23 @@ void launch_expval_finish(const double* partial, int64_t slots, int nterm, int b
   k_expval_finish<<<(unsigned)((items + 127) / 128), 128, 0, s>>>(partial, slots, nterm, blocks, xmask, ny, out);
 }
 
-void launch_cumsum_seq(int c64, const void* amps, int n, double* cdf, cudaStream_t s) {
-  if (c64) k_cumsum_seq<float><<<1, 1, 0, s>>>((const float2*)amps, 1ll << n, cdf);
-  else k_cumsum_seq<double><<<1, 1, 0, s>>>((const double2*)amps, 1ll << n, cdf);
+int64_t cdf_blocks(int n) { return ((1ll << n) + kCdfBlock - 1) / kCdfBlock; }
+
+void launch_cumsum_seq(int c64, const void* amps, int n, double* ends, cudaStream_t s) {
+  if (c64) k_cumsum_blocks<float><<<1, 1, 0, s>>>((const float2*)amps, 1ll << n, ends);
+  else k_cumsum_blocks<double><<<1, 1, 0, s>>>((const double2*)amps, 1ll << n, ends);
 }
 
-void launch_static_search(const double* cdf, int n, uint64_t seed, int64_t shot_begin, int64_t count,
-                          const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits,
+void launch_static_search(int c64, const void* amps, const double* ends, int n, uint64_t seed, int64_t shot_begin,
+                          int64_t count, const int32_t* mq, const int32_t* mb, int nmeas, int nwords, uint64_t* bits,
                           cudaStream_t s) {
-  k_static_search<<<(unsigned)((count + 127) / 128), 128, 0, s>>>(cdf, n, seed, shot_begin, count, mq, mb, nmeas,
-                                                                 nwords, bits);
+  const unsigned g = (unsigned)((count + 127) / 128);
+  if (c64)
+    k_static_search<float><<<g, 128, 0, s>>>((const float2*)amps, ends, n, seed, shot_begin, count, mq, mb, nmeas,
+                                             nwords, bits);
+  else
+    k_static_search<double><<<g, 128, 0, s>>>((const double2*)amps, ends, n, seed, shot_begin, count, mq, mb, nmeas,
+                                              nwords, bits);
 }
 
 }  // namespace qsb

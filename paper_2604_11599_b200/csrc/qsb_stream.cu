@@ -347,6 +347,8 @@ __global__ void __launch_bounds__(kDT) k_decide(StreamArgs a, RegionDesc rd) {
     }
     c.draws++;
     int outcome = u < p1 ? 1 : 0;
+    if (a.hbits && c.draws <= 64 * a.hwords)  // exact outcome history (dedup verification)
+      a.hbits[slot * a.hwords + ((c.draws - 1) >> 6)] |= (uint64_t)outcome << ((c.draws - 1) & 63);
     double pout = outcome ? p1 : 1.0 - p1;
     if (fabs(u - p1) < tol && a.tie_count) atomicAdd(a.tie_count, 1ull);
     if (pout < 1e-15) {
@@ -405,9 +407,14 @@ __global__ void k_dedup_regroup(StreamArgs a, int32_t* new_rep, int32_t* copy_sr
   if (c.status == 0) {
     for (int64_t t = 0; t < s; ++t) {
       const TrajCtl& o = a.ctl[t];
-      if (o.status == 0 && o.hist == c.hist) {
-        r = (int32_t)t;
-        break;
+      if (o.status == 0 && o.hist == c.hist && o.draws == c.draws) {
+        // the 64-bit hash is only a filter: merge on the exact outcome history
+        bool same = true;
+        for (int w = 0; w < a.hwords && same; ++w) same = a.hbits[t * a.hwords + w] == a.hbits[s * a.hwords + w];
+        if (same) {
+          r = (int32_t)t;
+          break;
+        }
       }
     }
   }
