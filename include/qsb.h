@@ -229,6 +229,12 @@ int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_
 int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
                          int32_t tile_qubits, int32_t low_qubits, int32_t reg_bits, int64_t* out);
 
+/* host-only: the streaming plan's passes (gates per pass, epilogue flag) with gate
+ * deferral past measurement regions on (1) or off (0); *npasses = number of passes.   */
+int32_t qsb_plan_passes(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                        int32_t tile_qubits, int32_t low_qubits, int32_t reg_bits, int32_t defer_gates,
+                        int64_t* gates_out, int32_t* epi_out, int32_t max_passes, int32_t* npasses);
+
 /* host-only: generate and NVRTC-compile (no device needed, nothing loaded) the
  * specialised pass kernels of a tape's streaming plan; returns QSB_OK or QSB_ERR_ARG
  * with the compiler log in qsb_last_error().  reg_bits = 3, 4 or 5 amplitude-register

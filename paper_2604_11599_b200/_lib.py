@@ -111,6 +111,7 @@ _SIGS = {
     "qsb_observe": (_I32, [_P, _I32, _P, _I64, _P, _P, _P, _P, _I32, _P, _P]),
     "qsb_debug_rng": (_I32, [_P, _U64, _I64, _I32, _P]),
     "qsb_plan_summary": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
+    "qsb_plan_passes": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _I32, ctypes.POINTER(_I32)]),
     "qsb_jit_selftest": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),
     "qsb_jit_nvrtc_version": (_I32, [_P, _P]),
     "qsb_fusion_stats": (_I32, [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P]),

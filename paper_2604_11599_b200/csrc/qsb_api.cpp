@@ -1612,6 +1612,25 @@ extern "C" int32_t qsb_plan_summary(const qsb_op* ops, int32_t nops, int32_t nqu
   return QSB_OK;
 }
 
+extern "C" int32_t qsb_plan_passes(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits, int32_t nparams,
+                                   int32_t tile_qubits, int32_t low_qubits, int32_t reg_bits, int32_t defer_gates,
+                                   int64_t* gates_out, int32_t* epi_out, int32_t max_passes, int32_t* npasses) {
+  TapeInfo t;
+  std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  StreamPlan P;
+  EngineOptions o;
+  o.defer_gates = defer_gates;
+  e = build_stream_plan(t, tile_qubits, low_qubits, reg_bits, swizzle_bits(low_qubits == 5), P, o);
+  if (!e.empty()) return fail(QSB_ERR_ARG, e);
+  *npasses = (int32_t)P.passes.size();
+  for (int i = 0; i < (int)P.passes.size() && i < max_passes; ++i) {
+    gates_out[i] = P.passes[i].gate_count;
+    epi_out[i] = P.passes[i].epi;
+  }
+  return QSB_OK;
+}
+
 extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqubits, int32_t nbits,
                                     int32_t nparams, int32_t precision, int32_t reg_bits, double* out) {
   const int c64 = precision == QSB_C64 ? 1 : 0;

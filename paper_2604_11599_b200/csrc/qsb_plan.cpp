@@ -247,6 +247,7 @@ struct Planner {
   bool pair_aware_ = P.opt.pair_aware != 0;
   bool phase_search_ = P.opt.phase_search != 0;
   bool block_condx_ = P.opt.block_condx != 0;
+  bool defer_ = P.opt.defer_gates != 0;
   std::vector<RegionBuild> regions;
 
   Planner(const TapeInfo& t_, int k_, int lowq_, int rb_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), rb(rb_), P(p) {}
@@ -499,41 +500,108 @@ struct Planner {
     P.steps.push_back({0, (int)P.passes.size() - 1});
   }
 
-  // greedy first-fit fusion of one gate region
+  // gates of `remaining` (in order) that one pass over tile set S absorbs: a gate joins when
+  // its targets are in S (diagonal gates anywhere) and no earlier rejected gate shares a
+  // qubit with it; grow = true lets S grow (greedy first fit) up to k qubits
+  int absorb(const std::vector<int>& remaining, uint64_t& S, bool grow, std::vector<int>* chosen,
+             std::vector<int>* rest) const {
+    uint64_t blocked = 0;
+    int taken = 0;
+    for (int gi : remaining) {
+      const DevOp& d = t.dev[gi];
+      if (taken == kMaxPassGates) {  // staging capacity of k_pass_reg
+        if (rest) rest->push_back(gi);
+        continue;
+      }
+      const uint64_t tm = (1ull << d.t0) | (d.t1 >= 0 ? (1ull << d.t1) : 0);
+      const uint64_t touched = tm | d.cm;
+      if (touched & blocked) {
+        if (rest) rest->push_back(gi);
+        blocked |= touched;
+        continue;
+      }
+      const uint64_t need = d.gclass == GC_DIAG ? 0 : (tm & ~S);
+      if (!need || (grow && popc(S | need) <= k)) {
+        S |= need;
+        if (chosen) chosen->push_back(gi);
+        ++taken;
+      } else {
+        if (rest) rest->push_back(gi);
+        blocked |= touched;
+      }
+    }
+    return taken;
+  }
+
+  // candidate tile sets of the next pass over `remaining`: the greedy first-fit set and
+  // every window of k - lowq consecutive qubits above the always-present low qubits (the
+  // light-cone shape of nearest-neighbour layers), ranked by the gates they absorb
+  std::vector<std::pair<int, uint64_t>> candidates(const std::vector<int>& remaining) const {
+    std::vector<std::pair<int, uint64_t>> c;
+    uint64_t g = low_mask();
+    const int ng = absorb(remaining, g, true, nullptr, nullptr);
+    c.push_back({ng, g});
+    const int w = k - lowq;
+    for (int a = lowq; w > 0 && a + w <= t.n; ++a) {
+      uint64_t S = low_mask() | (((w >= 64) ? ~0ull : ((1ull << w) - 1)) << a);
+      if (S == g) continue;
+      const int nabs = absorb(remaining, S, false, nullptr, nullptr);
+      if (nabs > 0) c.push_back({nabs, S});
+    }
+    std::stable_sort(c.begin(), c.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    return c;
+  }
+
+  // one gate region -> passes, by a small beam search over the tile set of each pass
+  // (kBeam partial schedules, kCand tile sets tried per step, ranked by the gates still
+  // left): the fewest passes found -- each pass is a full read + write of every state
   void flush(std::vector<int>& buf, int epi_region) {
     if (buf.empty()) {
       if (epi_region >= 0) emit_pass(low_mask(), {}, epi_region);
       return;
     }
-    std::vector<int> remaining = buf;
-    while (!remaining.empty()) {
-      uint64_t S = low_mask();
-      uint64_t blocked = 0;
-      std::vector<int> chosen, rest;
-      for (int gi : remaining) {
-        const DevOp& d = t.dev[gi];
-        if ((int)chosen.size() == kMaxPassGates) {  // staging capacity of k_pass_reg
-          rest.push_back(gi);
-          continue;
-        }
-        uint64_t tm = (1ull << d.t0) | (d.t1 >= 0 ? (1ull << d.t1) : 0);
-        uint64_t touched = tm | d.cm;
-        if (touched & blocked) {
-          rest.push_back(gi);
-          blocked |= touched;
-          continue;
-        }
-        uint64_t need = d.gclass == GC_DIAG ? 0 : (tm & ~S);
-        if (popc(S | need) <= k) {
-          S |= need;
-          chosen.push_back(gi);
-        } else {
-          rest.push_back(gi);
-          blocked |= touched;
+    constexpr int kBeam = 12, kCand = 8;
+    struct Sched {
+      std::vector<uint64_t> sets;
+      std::vector<int> remaining;
+    };
+    std::vector<Sched> beam{Sched{{}, buf}};
+    Sched done;
+    bool found = false;
+    while (!found) {
+      std::vector<Sched> next;
+      for (const Sched& st : beam) {
+        auto cands = candidates(st.remaining);
+        for (int ci = 0; ci < (int)cands.size() && ci < kCand; ++ci) {
+          Sched ns;
+          ns.sets = st.sets;
+          uint64_t S = cands[ci].second;
+          std::vector<int> chosen;
+          absorb(st.remaining, S, false, &chosen,
+                 &ns.remaining);
+          if (chosen.empty()) continue;
+          ns.sets.push_back(S);
+          next.push_back(std::move(ns));
         }
       }
-      bool last = rest.empty();
-      emit_pass(S, chosen, last ? epi_region : -1);
+      if (next.empty()) break;  // cannot happen: the first gate of a region always fits
+      std::stable_sort(next.begin(), next.end(),
+                       [](const Sched& a, const Sched& b) { return a.remaining.size() < b.remaining.size(); });
+      if (next[0].remaining.empty()) {
+        done = std::move(next[0]);
+        found = true;
+        break;
+      }
+      if ((int)next.size() > kBeam) next.resize(kBeam);
+      beam.swap(next);
+    }
+    // replay the chosen tile sets
+    std::vector<int> remaining = buf;
+    for (size_t i = 0; i < done.sets.size(); ++i) {
+      uint64_t S = done.sets[i];
+      std::vector<int> chosen, rest;
+      absorb(remaining, S, false, &chosen, &rest);
+      emit_pass(S, chosen, rest.empty() ? epi_region : -1);
       remaining.swap(rest);
     }
     buf.clear();
@@ -550,14 +618,57 @@ struct Planner {
     return true;
   }
 
+  // Gates of the region before a measurement region that touch none of its qubits (M:
+  // measured / reset qubits, descriptor-gate qubits) commute with it: the projection, the
+  // renormalisation, the lazy X frame and the marginal of M are all unchanged by a unitary
+  // on the other qubits.  Such an unguarded gate is DEFERRED past the region into the next
+  // gate region when it also commutes with every later gate that stays (disjoint
+  // supports), so the epilogue pass carries only the measured qubits' light cone and the
+  // deferred gates fill the next region's passes (DYN20: one state pass per round less).
+  void split_deferred(const std::vector<int>& pre, uint64_t M, std::vector<int>& kept, std::vector<int>& deferred) {
+    uint64_t after = M;  // supports of the region and of the kept gates later in order
+    std::vector<char> keep(pre.size(), 1);
+    for (int i = (int)pre.size() - 1; i >= 0; --i) {
+      const DevOp& d = t.dev[pre[i]];
+      const uint64_t sup = (1ull << d.t0) | (d.t1 >= 0 ? (1ull << d.t1) : 0) | d.cm;
+      if (defer_ && d.guard < 0 && !(sup & after)) {
+        keep[i] = 0;
+        continue;
+      }
+      after |= sup;
+    }
+    kept.clear();
+    deferred.clear();
+    for (size_t i = 0; i < pre.size(); ++i) (keep[i] ? kept : deferred).push_back(pre[i]);
+  }
+
   std::string run() {
     P.guard_gates.assign(std::max(1, t.nguards), 0);
     regions.emplace_back();  // R0: guards evaluated before the first measurement
     P.steps.push_back({1, 0});
     int cur = 0;
     bool meas_mode = false;
-    std::vector<int> buf;
+    std::vector<int> buf;   // gates since the last region
+    std::vector<int> pre;   // gates before the open region (flushed when it closes)
+    int open_region = -1;   // measurement region still collecting ops
     std::vector<int> path;
+    auto close_region = [&]() {
+      if (open_region < 0) return;
+      const RegionBuild& R = regions[open_region];
+      uint64_t M = 0;
+      for (int q : R.mq) M |= 1ull << q;
+      for (const DevOp& d : R.ops)
+        if (d.kind == QSB_OP_GATE) M |= (1ull << d.t0) | d.cm;
+      std::vector<int> kept, deferred;
+      split_deferred(pre, M, kept, deferred);
+      flush(kept, open_region);
+      P.steps.push_back({1, open_region});
+      // deferred gates run first in the next gate region (relative order kept)
+      deferred.insert(deferred.end(), buf.begin(), buf.end());
+      buf.swap(deferred);
+      pre.clear();
+      open_region = -1;
+    };
     for (int i = 0; i < (int)t.dev.size(); ++i) {
       const DevOp& d = t.dev[i];
       switch (d.kind) {
@@ -582,11 +693,13 @@ struct Planner {
             if (!known && (int)mq.size() == kMaxMeasureRegion) fresh = true;
           }
           if (fresh) {
+            close_region();  // a previous region still open (back to back, full M)
             regions.emplace_back();
             int r = (int)regions.size() - 1;
             regions[r].desc.has_marginal = 1;
-            flush(buf, r);
-            P.steps.push_back({1, r});
+            pre.swap(buf);
+            buf.clear();
+            open_region = r;
             cur = r;
             meas_mode = true;
           }
@@ -601,11 +714,13 @@ struct Planner {
             regions[cur].desc.desc_gates++;
             break;
           }
+          if (meas_mode) close_region();
           meas_mode = false;
           buf.push_back(i);
           break;
       }
     }
+    close_region();
     flush(buf, -1);
     return finish();
   }
@@ -710,6 +825,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "minblocks") minblocks = v;
   else if (key == "edge_x") edge_x = v;
   else if (key == "ctas_per_sm") ctas_per_sm = v;
+  else if (key == "defer_gates") defer_gates = v;
   else return false;
   return true;
 }
