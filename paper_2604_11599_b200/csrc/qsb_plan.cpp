@@ -624,7 +624,9 @@ struct Planner {
   // on the other qubits.  Such an unguarded gate is DEFERRED past the region into the next
   // gate region when it also commutes with every later gate that stays (disjoint
   // supports), so the epilogue pass carries only the measured qubits' light cone and the
-  // deferred gates fill the next region's passes (DYN20: one state pass per round less).
+  // deferred gates fill the next region's passes.  Option defer_gates (default off):
+  // measured on B200 with the beam-search tiling, DYN20 c128 3378 -> 2907 shots/s and
+  // RDC30 d40 696 -> 817 ms with it on (same pass counts, heavier epilogue passes).
   void split_deferred(const std::vector<int>& pre, uint64_t M, std::vector<int>& kept, std::vector<int>& deferred) {
     uint64_t after = M;  // supports of the region and of the kept gates later in order
     std::vector<char> keep(pre.size(), 1);

@@ -52,7 +52,7 @@ struct EngineOptions {
   int minblocks = 2;          // CTAs per SM the register budget of a pass kernel targets
   int edge_x = 1;             // conditional X gates at a phase edge as slot-base XORs
   int ctas_per_sm = 0;        // cap of the persistent pass grid per SM (0: occupancy)
-  int defer_gates = 1;        // gates commuting with a measurement region run after it
+  int defer_gates = 0;        // gates commuting with a measurement region run after it (measured slower: off)
   uint64_t key() const {
     const int v[] = {pair_aware, phase_search, block_condx, inline_phases, inline_min_gates, ffma2, packed_gates,
                      last_direct, last_direct_maxlow, minblocks, edge_x, ctas_per_sm, defer_gates};
