@@ -6,6 +6,9 @@ headline cfg 2 line of the driver contract).  One JSON line per config.
   cfg3  VQE24: 24-qubit HEA, 8 layers, 200-term Hamiltonian, points batched -- observe()
   cfg4  RDC30: 30-qubit random dynamic circuit, one trajectory, complex128 and complex64
   cfg5  sliced execution (emulated on one GPU: 8 slices), RDC with 3 global qubits
+  cpu1 / cpu3 / cpu4  the REFERENCE CPU path (baseline/_ref) on this host's
+        cores for cfg 1, 3 and 4 (W processes, one BLAS thread each; cfg 3 and 4 are bounded
+        samples, extrapolated and labelled so)
 
     python bench_configs.py [--only cfg1,cfg3] [--vqe-points 64] [--rdc-depth 200]
 """
@@ -147,6 +150,104 @@ def cfg5_single(args):
            "hbm_gbs_pass": st["pass_bytes"] / (st["pass_ms"] / 1e3) / 1e9, "key": tape.keys(words)[0]})
 
 
+# ---------------------------------------------------------------------------
+# reference CPU baselines (the unmodified qasm2cudaq from baseline/_ref)
+# ---------------------------------------------------------------------------
+
+REF = os.path.join(REPO, "baseline", "_ref")
+
+
+def _ref_modules():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    from qasm2cudaq import kir, sim, suites
+
+    return kir, sim, suites
+
+
+def _ref_ff(args):
+    kir, rsim, suites = _ref_modules()
+    from paper_2604_11599_b200 import workloads
+
+    src = dict(workloads.ff_suite())[args]
+    b = kir.bind(suites.compile_source(src[0]), [])
+    t0 = time.perf_counter()
+    h = rsim.sample(b, 1024, 1234)
+    return args, time.perf_counter() - t0, h.counts
+
+
+def _ref_vqe_point(p):
+    kir, rsim, suites = _ref_modules()
+    from paper_2604_11599_b200 import workloads
+
+    k = suites.compile_source(workloads.vqe_ansatz()[0])
+    ham = workloads.vqe_hamiltonian()
+    pt = workloads.vqe_points(4096)[p]
+    t0 = time.perf_counter()
+    sv = rsim.statevector(kir.bind(k, [float(x) for x in pt]))
+    e = 0.0
+    for c, w in ham:
+        e += c * rsim.expval_pauli(sv, w)
+    return p, time.perf_counter() - t0, e
+
+
+def host_cores() -> int:
+    return os.cpu_count() or 1
+
+
+def cpu1(args):
+    """cfg 1 in full: the six feedforward circuits, 1024 shots each, one circuit per process."""
+    import multiprocessing as mp
+
+    names = list(__import__("paper_2604_11599_b200.workloads", fromlist=["ff_suite"]).ff_suite())
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(min(len(names), host_cores())) as pool:
+        res = pool.map(_ref_ff, names)
+    wall = time.perf_counter() - t0
+    _emit({"config": "cpu1 reference qasm2cudaq (baseline/_ref) sim.sample, FF suite 1024 shots x 6 circuits",
+           "cores": min(len(names), host_cores()), "wall_s": wall, "shots_per_s": 6 * 1024 / wall,
+           "per_circuit_s": {n: dt for n, dt, _ in res}, "kind": "reference (full run)"})
+
+
+def cpu3(args):
+    """cfg 3 sample: one VQE24 point (statevector + 200 expval_pauli) per process, W processes;
+    extrapolated to the 4096-point sweep."""
+    import multiprocessing as mp
+
+    W = host_cores()
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(W) as pool:
+        res = pool.map(_ref_vqe_point, list(range(W)))
+    wall = time.perf_counter() - t0
+    _emit({"config": "cpu3 reference qasm2cudaq (baseline/_ref) VQE24 statevector + 200 expval_pauli per point",
+           "cores": W, "points": W, "wall_s": wall, "points_per_s": W / wall,
+           "per_point_s_median": sorted(dt for _, dt, _ in res)[W // 2],
+           "extrapolated_4096_points_h": 4096 / (W / wall) / 3600, "kind": "reference (sample, extrapolated)"})
+
+
+def cpu4(args):
+    """cfg 4 sample: the reference's apply_gate on a 30-qubit complex128 state for the first
+    `--cpu-gates` gates of RDC30 (one process: a single trajectory does not parallelise in
+    the reference), extrapolated per gate to the ~9000 gates of depth 200."""
+    kir, rsim, suites = _ref_modules()
+    from paper_2604_11599_b200 import workloads
+
+    src, k = workloads.rdc_circuit()
+    rk = suites.compile_source(src)
+    gates = [op for op in rk.body if type(op).__name__ == "Gate"][: args.cpu_gates]
+    st = rsim.StateVector.zero(30)
+    t0 = time.perf_counter()
+    for op in gates:
+        rsim.apply_gate(st, op, ())
+    dt = time.perf_counter() - t0
+    total_gates = sum(1 for op in k.body if type(op).__name__ == "Gate")
+    _emit({"config": "cpu4 reference qasm2cudaq (baseline/_ref) apply_gate at 30 qubits complex128 (RDC30 gates)",
+           "cores": 1, "gates_timed": len(gates), "s_per_gate": dt / len(gates),
+           "extrapolated_trajectory_h": dt / len(gates) * total_gates / 3600, "gates_in_trajectory": total_gates,
+           "kind": "reference (sample, extrapolated; measures not included)"})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,cfg5,cfg5_single")
@@ -154,8 +255,10 @@ def main():
     ap.add_argument("--vqe-points", type=int, default=64)
     ap.add_argument("--rdc-depth", type=int, default=200)
     ap.add_argument("--sliced-qubits", type=int, default=26)
+    ap.add_argument("--cpu-gates", type=int, default=12)
     args = ap.parse_args()
-    table = {"cfg1": cfg1, "cfg2": cfg2_c64, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5, "cfg5_single": cfg5_single}
+    table = {"cfg1": cfg1, "cfg2": cfg2_c64, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5, "cfg5_single": cfg5_single,
+             "cpu1": cpu1, "cpu3": cpu3, "cpu4": cpu4}
     for name in args.only.split(","):
         table[name](args)
 
