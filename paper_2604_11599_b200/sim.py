@@ -309,9 +309,8 @@ def _pred_record(rec, pred, offsets) -> None:
     else:
         if width > 64:
             raise BackendError(f"register predicates are limited to 64 bits (register {pred.register!r} has {width})")
-        if width == 0:  # empty register reads 0
-            rec["pred_bit"], rec["pred_width"] = 0, 0
-        rec["pred_bit"], rec["pred_width"] = base, width
+        # an empty register (width 0) reads 0: no bits are gathered
+        rec["pred_bit"], rec["pred_width"] = (0, 0) if width == 0 else (base, width)
     cmp, rhs = pred.comparator, int(pred.rhs)
     if cmp == "truthy":
         rec["pred_cmp"], rec["pred_rhs"] = _lib.CMP["truthy"], 0

@@ -514,3 +514,20 @@ def test_rdc30_full_size_properties():
     for q in range(28):
         z = sim.expval_pauli(st, "".join("Z" if i == q else "I" for i in range(28)))
         assert z >= 1.0 - 1e-10, (q, z)
+
+
+def test_compiled_tape_released_with_its_kernel():
+    """the tape cache must not keep a kernel (and its device tape, plans and
+    NVRTC modules) alive -- deleting the kernel drops its cache entry."""
+    import gc
+    import weakref
+
+    k = workloads.random_static(6, 20, seed=3)
+    sim.statevector(ir.bind(k, []))
+    key = (id(k), sim._ctx().device)
+    assert key in sim._tape_cache
+    ref = weakref.ref(k)
+    del k
+    gc.collect()
+    assert ref() is None
+    assert key not in sim._tape_cache
