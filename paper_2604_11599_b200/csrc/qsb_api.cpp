@@ -47,6 +47,7 @@ struct qsb_tape_s {
   DevBuf d_dev, d_matsrc, d_mats;  // d_mats: literal-only matrix table (no ParamRef angles)
   std::map<std::pair<int, uint64_t>, std::unique_ptr<PlanDev>> plans;  // (geometry, engine options)
   std::unique_ptr<qsb_tape_s> gates_only;          // static sampling view
+  std::unique_ptr<qsb_tape_s> phase_free;          // observe() view: global phases dropped
 };
 
 namespace {
@@ -1025,6 +1026,7 @@ int32_t qsb_tape_destroy(qsb_tape tp) {
   cudaStreamSynchronize(tp->ctx->stream);
   std::vector<qsb_tape> all = {tp};
   if (tp->gates_only) all.push_back(tp->gates_only.get());
+  if (tp->phase_free) all.push_back(tp->phase_free.get());
   for (qsb_tape t : all) {
     t->d_dev.release();
     t->d_matsrc.release();
@@ -1494,9 +1496,53 @@ int32_t qsb_sample_counts(qsb_tape tp, int32_t precision, const double* params, 
   return check_sticky();
 }
 
-int32_t qsb_observe(qsb_tape tp, int32_t precision, const double* params, int64_t npoints, const uint64_t* xmask,
+namespace {
+// observe() only needs <psi|P|psi>, which a global phase of psi does not change: the
+// ParamRef rz(theta) = e^{-i theta/2} diag(1, e^{i theta}) of the view is p(theta) (its
+// adjoint p(-theta)), a diagonal with a unit |0> entry that the pass kernels apply as one
+// complex scale of the |1> amplitude instead of two (VQE24: 192 of the 568 gates).
+int phase_free_view(qsb_tape tp, qsb_tape* out) {
+  if (tp->phase_free) {
+    *out = tp->phase_free.get();
+    return QSB_OK;
+  }
+  auto* v = new qsb_tape_s();
+  v->ctx = tp->ctx;
+  v->info = tp->info;
+  bool changed = false;
+  for (MatSrc& m : v->info.mats)
+    if (m.base == QSB_G_RZ && !m.has_matrix) {
+      m.base = QSB_G_P;
+      changed = true;
+    }
+  if (!changed) {
+    delete v;
+    *out = tp;
+    return QSB_OK;
+  }
+  for (DevOp& d : v->info.dev)
+    if (d.kind == QSB_OP_GATE && d.gclass == GC_DIAG && v->info.mats[d.mat].base == QSB_G_P) d.diag_one0 = 1;
+  int rc = upload_tape_device(v);
+  if (rc) {
+    delete v;
+    return rc;
+  }
+  tp->phase_free.reset(v);
+  *out = v;
+  return QSB_OK;
+}
+}  // namespace
+
+int32_t qsb_observe(qsb_tape tp_in, int32_t precision, const double* params, int64_t npoints, const uint64_t* xmask,
                     const uint64_t* zmask, const int32_t* ny, const double* coef, int32_t nterms, double* energies_out,
                     double* term_out) {
+  if (tp_in->info.top_level_dynamic) return fail(QSB_ERR_DYNAMIC, "observe needs a static kernel");
+  qsb_tape tp = tp_in;
+  {
+    DeviceGuard g0(tp_in->ctx->device);
+    int rc0 = phase_free_view(tp_in, &tp);
+    if (rc0) return rc0;
+  }
   const TapeInfo& t = tp->info;
   if (t.top_level_dynamic) return fail(QSB_ERR_DYNAMIC, "observe needs a static kernel");
   if (npoints < 1) return fail(QSB_ERR_ARG, "npoints must be >= 1");
