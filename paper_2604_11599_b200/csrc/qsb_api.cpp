@@ -1509,19 +1509,25 @@ int phase_free_view(qsb_tape tp, qsb_tape* out) {
   auto* v = new qsb_tape_s();
   v->ctx = tp->ctx;
   v->info = tp->info;
+  // only UNcontrolled rz: under a control the phase e^{-i theta/2} is relative, not global
+  std::vector<int> uses(v->info.mats.size(), 0);
+  for (const DevOp& d : v->info.dev)
+    if (d.kind == QSB_OP_GATE && d.mat >= 0) uses[d.mat]++;
   bool changed = false;
-  for (MatSrc& m : v->info.mats)
+  for (DevOp& d : v->info.dev) {
+    if (d.kind != QSB_OP_GATE || d.gclass != GC_DIAG || d.cm != 0 || d.mat < 0 || uses[d.mat] != 1) continue;
+    MatSrc& m = v->info.mats[d.mat];
     if (m.base == QSB_G_RZ && !m.has_matrix) {
       m.base = QSB_G_P;
+      d.diag_one0 = 1;
       changed = true;
     }
+  }
   if (!changed) {
     delete v;
     *out = tp;
     return QSB_OK;
   }
-  for (DevOp& d : v->info.dev)
-    if (d.kind == QSB_OP_GATE && d.gclass == GC_DIAG && v->info.mats[d.mat].base == QSB_G_P) d.diag_one0 = 1;
   int rc = upload_tape_device(v);
   if (rc) {
     delete v;
