@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstddef>
 #include <cstring>
+#include <chrono>
+#include <future>
 #include <map>
 #include <memory>
 #include <string>
@@ -31,6 +33,7 @@ namespace {
 
 struct PlanDev {
   StreamPlan plan;
+  std::future<JitJobs> pending;  // jit_async: NVRTC running in the background
   DevBuf gates, rops, guard_gates, phases, phase_gates;
   std::vector<JitKernel> jit;  // NVRTC-specialised kernel per pass (empty: generic kernel)
   std::vector<double> pflops;  // floating-point operations per state of each pass
@@ -93,13 +96,25 @@ int upload_tape_device(qsb_tape tp) {
 
 int reg_bits(qsb_ctx ctx) { return (int)ctx->opt_reg_bits; }  // amplitudes per thread = 2^reg_bits
 
+// jit_async: the background NVRTC compile of a plan finished -> load its kernels (this thread)
+void finish_async_jit(qsb_tape tp, PlanDev* pd, int c64) {
+  if (!pd->pending.valid() || pd->pending.wait_for(std::chrono::seconds(0)) != std::future_status::ready) return;
+  JitJobs J = pd->pending.get();
+  pd->jit_error = jit_load(tp->info, pd->plan, c64, J, pd->jit, &pd->jit_ms, &pd->jit_compiled, &pd->jit_cached);
+  if (!pd->jit_error.empty()) pd->jit.clear();
+}
+
 int get_plan(qsb_tape tp, int c64, int k, int lowq, int rb, PlanDev** out) {
   const bool want_jit = tp->ctx->opt_jit && tp->info.n >= tp->ctx->opt_jit_min;
-  const bool fuse = tp->ctx->opt_fuse != 0;
-  int key = ((((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0)) * 2 + (fuse ? 1 : 0)) * 2 + c64;
+  // jit_async: the generic kernel runs until the specialised kernels are compiled; fusion is
+  // off for such plans so both kernels give bit-identical results (deterministic whichever ran)
+  const bool async = want_jit && tp->ctx->opt_jit_async != 0;
+  const bool fuse = tp->ctx->opt_fuse != 0 && !async;
+  int key = (((((k * 64 + lowq) * 8 + rb) * 2 + (want_jit ? 1 : 0)) * 2 + (fuse ? 1 : 0)) * 2 + c64) * 2 + (async ? 1 : 0);
   const std::pair<int, uint64_t> pkey(key, tp->ctx->eopt.key());
   auto it = tp->plans.find(pkey);
   if (it != tp->plans.end()) {
+    if (async) finish_async_jit(tp, it->second.get(), c64);
     *out = it->second.get();
     return QSB_OK;
   }
@@ -126,7 +141,11 @@ int get_plan(qsb_tape tp, int c64, int k, int lowq, int rb, PlanDev** out) {
   pd->pflops.assign(P.passes.size(), 0.0);
   for (size_t i = 0; i < P.passes.size(); ++i)
     if (P.passes[i].phase_count) pd->pflops[i] = pass_flops(tp->info, P, (int)i);
-  if (want_jit && P.rb) {
+  if (want_jit && P.rb && async) {
+    pd->pending = std::async(std::launch::async, [info = tp->info, plan = P, c64] {
+      return jit_prepare(info, plan, c64, false);
+    });
+  } else if (want_jit && P.rb) {
     pd->jit_error = jit_build(tp->info, P, c64, fuse, pd->jit, &pd->jit_ms, &pd->jit_compiled, &pd->jit_cached);
     if (!pd->jit_error.empty()) pd->jit.clear();  // generic kernel for every pass
   }
@@ -487,6 +506,7 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
+  else if (k == "jit_async") ctx->opt_jit_async = value;  // NVRTC in the background, generic kernel meanwhile
   else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");

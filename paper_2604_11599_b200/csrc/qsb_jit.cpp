@@ -708,25 +708,21 @@ void write_cache(const std::string& path, const std::vector<char>& cubin) {
 }
 }  // namespace
 
-std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, std::vector<JitKernel>& out,
-                      double* compile_ms, int* compiled, int* cached) {
+// host half of jit_build: generate every pass's source, read the cubin cache, NVRTC-compile
+// the misses in parallel and write them back.  No CUDA calls: safe on a background thread.
+JitJobs jit_prepare(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse) {
+  JitJobs out;
   auto t0 = std::chrono::steady_clock::now();
-  out.assign(P.passes.size(), JitKernel());
-  *compiled = *cached = 0;
-  if (!P.rb) return "";
-  if (!jit_available()) return "libnvrtc not available";
+  if (!P.rb) return out;
+  if (!jit_available()) {
+    out.error = "libnvrtc not available";
+    return out;
+  }
   const std::string dir = cache_dir();
-  struct Job {
-    int pass;
-    std::string src, path;
-    std::vector<char> cubin;
-    std::string log;
-    bool ok = false, from_cache = false;
-  };
-  std::vector<Job> jobs;
+  std::vector<JitJob>& jobs = out.jobs;
   for (int i = 0; i < (int)P.passes.size(); ++i) {
     if (P.passes[i].phase_count == 0) continue;
-    Job j;
+    JitJob j;
     j.pass = i;
     j.src = jit_source(t, P, i, c64, fuse);
     std::string key = j.src;
@@ -748,14 +744,26 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
   for (unsigned w = 0; w < nthreads; ++w)
     pool.emplace_back([&] {
       for (size_t i = next++; i < jobs.size(); i = next++) {
-        Job& j = jobs[i];
+        JitJob& j = jobs[i];
         if (j.ok) continue;
         j.ok = compile_one(j.src, j.cubin, j.log);
         if (j.ok) write_cache(j.path, j.cubin);
       }
     });
   for (auto& th : pool) th.join();
-  for (Job& j : jobs) {
+  out.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return out;
+}
+
+// device half: load the cubins (on the calling thread; a damaged cache entry is recompiled)
+std::string jit_load(const TapeInfo& t, const StreamPlan& P, int c64, JitJobs& J, std::vector<JitKernel>& out,
+                     double* compile_ms, int* compiled, int* cached) {
+  auto t0 = std::chrono::steady_clock::now();
+  out.assign(P.passes.size(), JitKernel());
+  *compiled = *cached = 0;
+  if (!J.error.empty()) return J.error;
+  std::vector<JitJob>& jobs = J.jobs;
+  for (JitJob& j : jobs) {
     if (!j.ok) {
       jit_release(out);
       return "NVRTC failed for pass " + std::to_string(j.pass) + ": " + j.log.substr(0, 2000);
@@ -807,9 +815,16 @@ std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse
     if (j.from_cache) (*cached)++;
     else (*compiled)++;
   }
-  *compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *compile_ms = J.ms + std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return "";
 }
+
+std::string jit_build(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, std::vector<JitKernel>& out,
+                      double* compile_ms, int* compiled, int* cached) {
+  JitJobs J = jit_prepare(t, P, c64, fuse);
+  return jit_load(t, P, c64, J, out, compile_ms, compiled, cached);
+}
+
 
 std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse, int* kernels, double* ms) {
   auto t0 = std::chrono::steady_clock::now();

@@ -26,6 +26,25 @@ void jit_nvrtc_version(int* major, int* minor);
 // true if a phase of the pass reads the per-item staged gates (see pass_persistent)
 bool pass_needs_stage(const TapeInfo& t, const StreamPlan& P, int pass);
 
+// one pass kernel's source / cubin (jit_prepare) before it is loaded (jit_load)
+struct JitJob {
+  int pass = -1;
+  std::string src, path;
+  std::vector<char> cubin;
+  std::string log;
+  bool ok = false, from_cache = false;
+};
+struct JitJobs {
+  std::vector<JitJob> jobs;
+  std::string error;
+  double ms = 0;
+};
+// host half (no CUDA calls; background-thread safe): sources, cache, parallel NVRTC
+JitJobs jit_prepare(const TapeInfo& t, const StreamPlan& P, int c64, bool fuse);
+// device half: load the cubins into modules / kernels
+std::string jit_load(const TapeInfo& t, const StreamPlan& P, int c64, JitJobs& jobs, std::vector<JitKernel>& out,
+                     double* compile_ms, int* compiled, int* cached);
+
 // Generates, compiles (parallel, cached by source hash in $QSB_JIT_CACHE or
 // /tmp/qsb_jit_cache) and loads one kernel per register-blocked pass of `P`.
 // out[i] stays empty for passes without phases.  Returns "" or an error.

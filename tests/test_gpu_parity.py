@@ -531,3 +531,34 @@ def test_compiled_tape_released_with_its_kernel():
     gc.collect()
     assert ref() is None
     assert key not in sim._tape_cache
+
+
+def test_jit_async_generic_first_then_specialised_bit_identical():
+    """Option jit_async: the first runs of a new tape use the generic kernel while NVRTC
+    compiles in the background, later runs the specialised kernels -- fusion is off for
+    such plans, so every run is bit-identical to the generic kernel (deterministic
+    whichever kernel ran), and the specialised kernels do arrive."""
+    import time
+
+    _, k = workloads.dyn_circuit(n=15, layers=10, every=5, nmeas=3, seed=77)
+    b = ir.bind(k, [])
+    with option("jit", 0, 1):
+        ref_words, _ = sim.sample_final_states(b, 32, 5, 2)
+    ctx = _lib.context()
+    ctx.set_option("jit_async", 1)
+    try:
+        _, k2 = workloads.dyn_circuit(n=15, layers=10, every=5, nmeas=3, seed=77)  # a fresh tape
+        b2 = ir.bind(k2, [])
+        seen = set()
+        for _ in range(60):
+            words, states = sim.sample_final_states(b2, 32, 5, 2)
+            np.testing.assert_array_equal(words, ref_words)
+            seen.add(sim.last_stats()["jit_passes"] > 0)
+            if True in seen:
+                break
+            time.sleep(1.0)
+        assert True in seen, "the background NVRTC kernels never arrived"
+        words, states = sim.sample_final_states(b2, 32, 5, 2)
+        np.testing.assert_array_equal(words, ref_words)
+    finally:
+        ctx.set_option("jit_async", 0)
