@@ -543,7 +543,8 @@ def test_jit_async_generic_first_then_specialised_bit_identical():
     _, k = workloads.dyn_circuit(n=15, layers=10, every=5, nmeas=3, seed=77)
     b = ir.bind(k, [])
     with option("jit", 0, 1):
-        ref_words, _ = sim.sample_final_states(b, 32, 5, 2)
+        ref_words, ref_states = sim.sample_final_states(b, 32, 5, 2)
+        ref_amps = [np.array(st.amps) for st in ref_states]
     ctx = _lib.context()
     ctx.set_option("jit_async", 1)
     try:
@@ -553,6 +554,8 @@ def test_jit_async_generic_first_then_specialised_bit_identical():
         for _ in range(60):
             words, states = sim.sample_final_states(b2, 32, 5, 2)
             np.testing.assert_array_equal(words, ref_words)
+            for st, ra in zip(states, ref_amps):
+                np.testing.assert_array_equal(st.amps, ra)
             seen.add(sim.last_stats()["jit_passes"] > 0)
             if True in seen:
                 break
