@@ -62,9 +62,12 @@ int tile_qubits(qsb_ctx ctx, int c64) {
   if (ctx->opt_tile > 0) return (int)std::min<int64_t>(ctx->opt_tile, kMaxTile);
   return 12;  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA
 }
-// contiguous low qubits of every tile: 256-byte runs by default (option low_qubits
-// overrides; shorter runs let a tile cover more qubits of a light cone)
-int low_qubits(qsb_ctx ctx, int c64) { return ctx->opt_lowq > 0 ? (int)ctx->opt_lowq : (c64 ? 5 : 4); }
+// contiguous low qubits of every tile: 3 (runs of 8 amplitudes: 128 B complex128, 64 B
+// complex64) by default -- measured on B200 with the beam-search tiling (round 2), the tile
+// covering one more qubit of the light cones beats the longer runs: DYN20 c128 3443 -> 3518
+// shots/s, c64 4951 -> 5286, RDC30 d40 c128 698 -> 681 ms, VQE24 c128 267 -> 271 points/s
+// (round 1's 256-byte runs: lowq 4 / 5).  Option low_qubits overrides.
+int low_qubits(qsb_ctx ctx, int c64) { return ctx->opt_lowq > 0 ? (int)ctx->opt_lowq : 3; }
 
 // Blocking copy ordered on the context's stream.  ctx->stream is non-blocking, so a plain
 // cudaMemcpy (legacy stream) neither waits for work queued on it nor -- for pageable
@@ -1711,7 +1714,7 @@ extern "C" int32_t qsb_jit_selftest(const qsb_op* ops, int32_t nops, int32_t nqu
   std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   StreamPlan P;
-  e = build_stream_plan(t, 12, c64 ? 5 : 4, reg_bits, swizzle_bits(c64), P);
+  e = build_stream_plan(t, 12, 3, reg_bits, swizzle_bits(c64), P);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   int nk = 0;
   double ms = 0;
@@ -1740,7 +1743,7 @@ extern "C" int32_t qsb_fusion_stats(const qsb_op* ops, int32_t nops, int32_t nqu
   std::string e = analyze_tape(ops, nops, nqubits, nbits, nparams, t);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   StreamPlan P;
-  e = build_stream_plan(t, 12, c64 ? 5 : 4, reg_bits, swizzle_bits(c64), P);
+  e = build_stream_plan(t, 12, 3, reg_bits, swizzle_bits(c64), P);
   if (!e.empty()) return fail(QSB_ERR_ARG, e);
   const int fail0 = fuse_check_failures();
   double st[6] = {0, 0, 0, 0, 0, 0};
