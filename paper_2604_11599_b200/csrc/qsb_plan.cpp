@@ -560,7 +560,7 @@ struct Planner {
       if (epi_region >= 0) emit_pass(low_mask(), {}, epi_region);
       return;
     }
-    constexpr int kBeam = 12, kCand = 8;
+    constexpr int kBeam = 64, kCand = 16;
     struct Sched {
       std::vector<uint64_t> sets;
       std::vector<int> remaining;
