@@ -552,15 +552,18 @@ struct Planner {
     return c;
   }
 
-  // one gate region -> passes, by a small beam search over the tile set of each pass
-  // (kBeam partial schedules, kCand tile sets tried per step, ranked by the gates still
-  // left): the fewest passes found -- each pass is a full read + write of every state
+  // one gate region -> passes, by a beam search over the tile set of each pass (kBeam
+  // partial schedules, kCand tile sets tried per step, ranked by the gates still left):
+  // the fewest passes found -- each pass is a full read + write of every state
   void flush(std::vector<int>& buf, int epi_region) {
     if (buf.empty()) {
       if (epi_region >= 0) emit_pass(low_mask(), {}, epi_region);
       return;
     }
-    constexpr int kBeam = 64, kCand = 16;
+    // beam width scaled to the region so planning stays ~linear in the gate count (64 x 16
+    // up to ~6k gates per region: DYN20 / RDC / VQE; a 100k-gate static region gets 4 x 8)
+    const int kBeam = (int)std::max<size_t>(4, std::min<size_t>(64, 400000 / std::max<size_t>(1, buf.size())));
+    const int kCand = kBeam >= 16 ? 16 : 8;
     struct Sched {
       std::vector<uint64_t> sets;
       std::vector<int> remaining;
