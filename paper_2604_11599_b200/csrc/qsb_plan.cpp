@@ -247,7 +247,7 @@ struct Planner {
   bool pair_aware_ = P.opt.pair_aware != 0;
   bool phase_search_ = P.opt.phase_search != 0;
   bool block_condx_ = P.opt.block_condx != 0;
-  bool defer_ = P.opt.defer_gates != 0;
+  int defer_from_ = P.opt.defer_gates;  // 0: off; r: defer past measurement regions r, r+1, ...
   std::vector<RegionBuild> regions;
 
   Planner(const TapeInfo& t_, int k_, int lowq_, int rb_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), rb(rb_), P(p) {}
@@ -630,13 +630,14 @@ struct Planner {
   // deferred gates fill the next region's passes.  Option defer_gates (default off):
   // measured on B200 with the beam-search tiling, DYN20 c128 3378 -> 2907 shots/s and
   // RDC30 d40 696 -> 817 ms with it on (same pass counts, heavier epilogue passes).
-  void split_deferred(const std::vector<int>& pre, uint64_t M, std::vector<int>& kept, std::vector<int>& deferred) {
+  void split_deferred(const std::vector<int>& pre, uint64_t M, bool defer, std::vector<int>& kept,
+                      std::vector<int>& deferred) {
     uint64_t after = M;  // supports of the region and of the kept gates later in order
     std::vector<char> keep(pre.size(), 1);
     for (int i = (int)pre.size() - 1; i >= 0; --i) {
       const DevOp& d = t.dev[pre[i]];
       const uint64_t sup = (1ull << d.t0) | (d.t1 >= 0 ? (1ull << d.t1) : 0) | d.cm;
-      if (defer_ && d.guard < 0 && !(sup & after)) {
+      if (defer && d.guard < 0 && !(sup & after)) {
         keep[i] = 0;
         continue;
       }
@@ -665,7 +666,7 @@ struct Planner {
       for (const DevOp& d : R.ops)
         if (d.kind == QSB_OP_GATE) M |= (1ull << d.t0) | d.cm;
       std::vector<int> kept, deferred;
-      split_deferred(pre, M, kept, deferred);
+      split_deferred(pre, M, defer_from_ > 0 && open_region >= defer_from_, kept, deferred);
       flush(kept, open_region);
       P.steps.push_back({1, open_region});
       // deferred gates run first in the next gate region (relative order kept)
