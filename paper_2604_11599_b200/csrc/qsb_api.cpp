@@ -509,7 +509,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
-  else if (k == "jit_async") ctx->opt_jit_async = value;  // NVRTC in the background, generic kernel meanwhile
+  else if (k == "jit_async") ctx->opt_jit_async = value;
+  else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles  // NVRTC in the background, generic kernel meanwhile
   else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
@@ -725,7 +726,7 @@ namespace {
 // tile set (greedy first fit, larger supports first); Z-only terms join the first group.
 int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t slots, const uint64_t* xm,
                        const uint64_t* zm, const int32_t* ny, int nterm, double* out_host) {
-  const int k = std::min(12, n), lowq = std::min(2, k);
+  const int k = std::min(12, n), lowq = std::min((int)(ctx->opt_ev_lowq > 0 ? ctx->opt_ev_lowq : 2), k);
   const uint64_t lowmask = (1ull << lowq) - 1;
   std::vector<int> order(nterm);
   for (int t = 0; t < nterm; ++t) order[t] = t;
