@@ -485,6 +485,7 @@ int32_t qsb_ctx_destroy(qsb_ctx ctx) {
                     &ctx->predrawn, &ctx->status, &ctx->counters, &ctx->misc, &ctx->misc2, &ctx->trace,
                     &ctx->dedup, &ctx->histbits, &ctx->shotwords, &ctx->histo})
     b->release();
+  for (auto& kv : ctx->ev_jit) cudaLibraryUnload((cudaLibrary_t)kv.second.first);
   for (auto e : ctx->pass_events) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_a);
   cudaEventDestroy(ctx->ev_b);
@@ -510,7 +511,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
   else if (k == "jit_async") ctx->opt_jit_async = value;
-  else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles  // NVRTC in the background, generic kernel meanwhile
+  else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles
+  else if (k == "expval_jit") ctx->opt_ev_jit = value;  // NVRTC-specialised Pauli reducer  // NVRTC in the background, generic kernel meanwhile
   else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
@@ -936,8 +938,68 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   }
   double* p_acc = ctx->misc.as<double>();
   double* p_tile = p_acc + acc_words;
-  for (const ExpvalGroup& g : acc_groups)
-    launch_expval_acc(c64, amps, n, slots, g, d_terms, d_maps, d_classes, p_acc, nterm, ctx->stream);
+  // NVRTC-specialised reducer per launch group (observe-sized jobs; compiled once per
+  // Hamiltonian grouping and cached per context and on disk), else the generic kernel
+  std::vector<void*> jk(acc_groups.size(), nullptr);
+  if (ctx->opt_jit && ctx->opt_ev_jit && n >= 16 && nterm >= 8 && !acc_groups.empty() && jit_available()) {
+    std::vector<std::string> srcs(acc_groups.size());
+    std::vector<size_t> keys(acc_groups.size());
+    std::vector<size_t> missing;
+    for (size_t gi = 0; gi < acc_groups.size(); ++gi) {
+      const ExpvalGroup& g = acc_groups[gi];
+      EvJitSpec sp;
+      sp.c64 = c64;
+      sp.lowq = lowq;
+      for (int mi = 0; mi < g.nmap; ++mi) {
+        const EvMap& em = dev_maps[g.map_begin + mi];
+        EvJitMap m{};
+        for (int b = 0; b < 8; ++b) m.tpos[b] = em.tpos[b];
+        for (int j = 0; j < 16; ++j) m.soff[j] = em.soff[j];
+        m.t0 = em.term_begin - g.term_begin;
+        m.nt = em.nterm;
+        sp.maps.push_back(m);
+      }
+      for (int t = 0; t < g.nterm; ++t) {
+        const ExpvalTerm& e = dev_terms[g.term_begin + t];
+        sp.terms.push_back(EvJitTerm{e.xr, e.zsig, e.zl, e.zg, e.ny, e.out});
+      }
+      srcs[gi] = ev_jit_source(sp) + "// smask " + std::to_string(g.smask) + "\n";
+      keys[gi] = std::hash<std::string>()(srcs[gi]);
+      auto it = ctx->ev_jit.find(keys[gi]);
+      if (it != ctx->ev_jit.end()) jk[gi] = it->second.second;
+      else missing.push_back(gi);
+    }
+    if (!missing.empty()) {
+      std::vector<std::string> ms;
+      for (size_t gi : missing) ms.push_back(srcs[gi]);
+      std::vector<JitKernel> built;
+      ev_jit_build(ms, built);  // failures leave kern null: the generic kernel runs
+      for (size_t i = 0; i < missing.size(); ++i)
+        if (built[i].kern) {
+          ctx->ev_jit[keys[missing[i]]] = {built[i].lib, built[i].kern};
+          jk[missing[i]] = built[i].kern;
+        }
+    }
+  }
+  for (size_t gi = 0; gi < acc_groups.size(); ++gi) {
+    const ExpvalGroup& g = acc_groups[gi];
+    if (!jk[gi]) {
+      launch_expval_acc(c64, amps, n, slots, g, d_terms, d_maps, d_classes, p_acc, nterm, ctx->stream);
+      continue;
+    }
+    const size_t amp = c64 ? 8 : 16;
+    auto up = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    const size_t smem = up((c64 ? 2 : 1) * amp * 4096) + up(sizeof(double) * 256 * (size_t)g.nterm) +
+                        up(sizeof(uint64_t) * (4096 >> lowq)) + up(sizeof(uint32_t) * (4096 >> (c64 ? 4 : 3))) +
+                        up(sizeof(uint64_t) * 32) + up(sizeof(uint32_t) * 2) + 16;
+    const int nchunks_i = nchunks;
+    const void* st_p = amps;
+    int n_i = n;
+    unsigned long long sm = g.smask;
+    int nt_i = nterm;
+    void* args[] = {(void*)&st_p, (void*)&n_i, (void*)&sm, (void*)&p_acc, (void*)&nt_i, (void*)&nchunks_i};
+    QSB_CUDA(cudaLaunchKernel(jk[gi], dim3((unsigned)(slots * nchunks)), dim3(256), args, smem, ctx->stream));
+  }
   for (const ExpvalGroup& g : dev_groups)
     if (g.nterm)
       launch_expval_tile(c64, amps, n, slots, g, d_terms, d_maps, p_tile, nterm, ctx->stream);

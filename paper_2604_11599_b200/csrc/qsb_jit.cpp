@@ -845,6 +845,259 @@ std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, bo
   return "";
 }
 
+
+// ---------------------------------------------------------------------------
+// NVRTC-specialised Pauli reducer: the generic k_expval_acc (qsb_expval.cu) with every
+// structural quantity a compile-time constant -- mapping thread positions and swizzled
+// register offsets, each class's register X pattern (only the product parts its terms
+// use), each term's register Z signs (add / subtract in the butterfly, no sign factors),
+// its thread-parity mask, out-of-tile Z mask and output index.  Per term and tile a thread
+// does 7 (diagonal: 15) add / subtract, one sign flip and one accumulator update.
+// ---------------------------------------------------------------------------
+
+std::string ev_jit_source(const EvJitSpec& S) {
+  const int T = (int)S.terms.size();
+  const int sbits = S.c64 ? 4 : 3;
+  std::ostringstream o;
+  for (const char* part : kJitPreludeParts) o << part;
+  o << "\ntypedef " << (S.c64 ? "float" : "double") << " R;\ntypedef " << (S.c64 ? "float2" : "double2") << " A;\n";
+  o << "__device__ __forceinline__ double sgnd(double x, uint32_t m) {\n"
+       "  return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)m << 32));\n}\n";
+  o << "__constant__ unsigned long long qsb_ev_zg[" << std::max(1, T) << "] = {";
+  for (int t = 0; t < T; ++t) o << (t ? ", " : "") << S.terms[t].zg << "ull";
+  if (!T) o << "0ull";
+  o << "};\n";
+  const int nbuf = S.c64 ? 2 : 1;
+  o << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsb_ev_jit(const A* __restrict__ states, int n, "
+       "unsigned long long smask, double* __restrict__ partial, int nterm_total, int nchunks) {\n";
+  o << "  constexpr int SB = " << sbits << ", K = 12, TL = 4096, LOWQ = " << S.lowq << ", NT = " << T
+    << ", NBUF = " << nbuf << ", TPC_MAX = 32;\n";
+  o << R"(  extern __shared__ __align__(16) unsigned char smem_raw[];
+  size_t off = 0;
+  auto carve = [&](size_t bytes) { unsigned char* p = smem_raw + off; off = (off + bytes + 15) & ~(size_t)15; return p; };
+  A* tiles = reinterpret_cast<A*>(carve(sizeof(A) * NBUF * TL));
+  double* acc = reinterpret_cast<double*>(carve(sizeof(double) * NT * 256));
+  uint64_t* hi_off = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * (TL >> LOWQ)));
+  uint32_t* swz = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * (TL >> SB)));
+  uint64_t* ibase = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * TPC_MAX));
+  uint32_t* tword = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * 2));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t qmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  const uint64_t lowm = (1ull << LOWQ) - 1;
+  const uint64_t shi = smask & ~lowm;
+  for (int h = tid; h < (TL >> LOWQ); h += 256) hi_off[h] = qsb::pdep64((uint64_t)h, shi);
+  const uint8_t* V = SB == 3 ? qsb::c_swz3 : qsb::c_swz4;
+  for (int h = tid; h < (TL >> SB); h += 256) {
+    uint32_t sw = 0;
+    for (int p = SB, hh = h; hh; ++p, hh >>= 1)
+      if (hh & 1) sw ^= V[p];
+    swz[h] = sw;
+  }
+  const uint64_t outmask = ~smask & qmask;
+  for (int i = tid; i < TPC_MAX; i += 256) ibase[i] = qsb::pdep64((uint64_t)i, outmask);
+  for (int i = tid; i < NT * 256; i += 256) acc[i] = 0.0;
+  __syncthreads();
+)";
+  // per-thread parity word: bit t = parity(thread's tile bits of t's mapping & zl_t) = parity(tid & TM_t)
+  o << "  const uint32_t pthread = 0u";
+  for (const EvJitMap& m : S.maps)
+    for (int t = m.t0; t < m.t0 + m.nt; ++t) {
+      uint32_t tm = 0;
+      for (int b = 0; b < 8; ++b)
+        if (S.terms[t].zl >> m.tpos[b] & 1) tm |= 1u << b;
+      if (tm) o << " | ((uint32_t)(__popc((uint32_t)tid & " << tm << "u) & 1) << " << t << ")";
+    }
+  o << ";\n";
+  o << R"(  const int ntl = n - K;
+  const int64_t ntiles = (int64_t)1 << ntl;
+  const int64_t slot = blockIdx.x / nchunks, chunk = blockIdx.x % nchunks;
+  const int64_t tpc = ntiles / nchunks, w0 = chunk * tpc;
+  const A* st = states + (slot << n);
+  const uint64_t Pt = ((uint64_t)tid & lowm) | hi_off[tid >> LOWQ];
+  const uint32_t St = qsb::swz_slot<SB>(swz, (uint32_t)tid);
+  const int hstep = 256 >> LOWQ;
+  const uint64_t my_zg = lane < NT ? qsb_ev_zg[lane < NT ? lane : 0] : 0ull;
+  const uint64_t base0 = qsb::pdep64((uint64_t)w0, outmask);
+  auto load = [&](int64_t i, A* dst_tile) {
+    const uint64_t base = base0 | ibase[i];
+#pragma unroll
+    for (int r = 0; r < TL / 256; ++r) {
+      const A* src = st + (base | Pt | hi_off[r * hstep]);
+      A* dst = dst_tile + (St ^ qsb::swz_slot<SB>(swz, (uint32_t)(r * 256)));
+      if (sizeof(A) == 16) qsb::cp_async16(dst, src);
+      else qsb::cp_async8(dst, src);
+    }
+    qsb::cp_async_commit();
+  };
+  load(0, tiles);
+  for (int64_t i = 0; i < tpc; ++i) {
+    if (NBUF == 2 && i + 1 < tpc) {
+      load(i + 1, tiles + ((i + 1) & 1) * TL);
+      qsb::cp_async_wait1();
+    } else {
+      qsb::cp_async_wait0();
+    }
+    if (warp == 0) {
+      const uint64_t base = base0 | ibase[i];
+      const uint32_t word = __ballot_sync(0xffffffffu, lane < NT && (__popcll(base & my_zg) & 1));
+      if (lane == 0) tword[i & 1] = word;
+    }
+    __syncthreads();
+    const A* tile = tiles + (NBUF == 2 ? (i & 1) * TL : 0);
+    const uint32_t pw = pthread ^ tword[i & 1];
+)";
+  auto acc_line = [&](int t, const std::string& s) {
+    o << "      acc[" << t << " * 256 + tid] += sgnd((double)(" << s << "), (pw << " << (31 - t) << ") & 0x80000000u);\n";
+  };
+  for (size_t mi = 0; mi < S.maps.size(); ++mi) {
+    const EvJitMap& m = S.maps[mi];
+    o << "    {  // mapping " << mi << "\n      const uint32_t tb = 0u";
+    for (int b = 0; b < 8; ++b) o << " | ((((uint32_t)tid >> " << b << ") & 1u) << " << m.tpos[b] << ")";
+    o << ";\n      const uint32_t sb = qsb::swz_slot<SB>(swz, tb);\n";
+    for (int j = 0; j < 16; ++j) o << "      const A v" << j << " = tile[sb ^ " << m.soff[j] << "u];\n";
+    // classes: runs of equal xr
+    int t = m.t0;
+    while (t < m.t0 + m.nt) {
+      const uint32_t xr = S.terms[t].xr;
+      int e = t;
+      bool need_re = false, need_im = false;
+      while (e < m.t0 + m.nt && S.terms[e].xr == xr) {
+        if (S.terms[e].ny & 1) need_im = true;
+        else need_re = true;
+        ++e;
+      }
+      o << "      {  // class xr " << xr << "\n";
+      if (xr == 0) {
+        for (int j = 0; j < 16; ++j)
+          o << "      const R q" << j << " = fma(v" << j << ".x, v" << j << ".x, v" << j << ".y * v" << j << ".y);\n";
+        for (int tt = t; tt < e; ++tt) {
+          // butterfly over the 4 register bits with the term's signs (zsig bit (1 << b))
+          std::vector<std::string> x(16);
+          for (int j = 0; j < 16; ++j) x[j] = "q" + std::to_string(j);
+          for (int b = 0; b < 4; ++b) {
+            const bool neg = S.terms[tt].zsig >> (1u << b) & 1;
+            std::vector<std::string> y;
+            for (size_t j = 0; j < x.size(); j += 2) y.push_back("(" + x[j] + (neg ? " - " : " + ") + x[j + 1] + ")");
+            x.swap(y);
+          }
+          acc_line(tt, x[0]);
+        }
+      } else {
+        const int top = 31 - __builtin_clz(xr);
+        int bits[3], nb = 0;
+        for (int b = 0; b < 4; ++b)
+          if (b != top) bits[nb++] = b;
+        for (int k = 0; k < 8; ++k) {
+          const int j = ((k & 1) << bits[0]) | (((k >> 1) & 1) << bits[1]) | (((k >> 2) & 1) << bits[2]);
+          const int jx = j ^ (int)xr;
+          if (need_re)
+            o << "      const R pr" << k << " = fma(v" << j << ".x, v" << jx << ".x, v" << j << ".y * v" << jx << ".y);\n";
+          if (need_im)
+            o << "      const R pi" << k << " = fma(v" << j << ".x, v" << jx << ".y, -v" << j << ".y * v" << jx << ".x);\n";
+        }
+        for (int tt = t; tt < e; ++tt) {
+          const char* pre = (S.terms[tt].ny & 1) ? "pi" : "pr";
+          std::vector<std::string> x(8);
+          for (int k = 0; k < 8; ++k) x[k] = std::string(pre) + std::to_string(k);
+          for (int lv = 0; lv < 3; ++lv) {
+            const bool neg = S.terms[tt].zsig >> (1u << bits[lv]) & 1;
+            std::vector<std::string> y;
+            for (size_t j = 0; j < x.size(); j += 2) y.push_back("(" + x[j] + (neg ? " - " : " + ") + x[j + 1] + ")");
+            x.swap(y);
+          }
+          acc_line(tt, x[0]);
+        }
+      }
+      o << "      }\n";
+      t = e;
+    }
+    o << "    }\n";
+  }
+  o << R"(    __syncthreads();
+    if (NBUF == 1 && i + 1 < tpc) load(i + 1, tiles);
+  }
+)";
+  o << "  const int outs[" << std::max(1, T) << "] = {";
+  for (int t = 0; t < T; ++t) o << (t ? ", " : "") << S.terms[t].out;
+  if (!T) o << "0";
+  o << "};\n";
+  o << R"(  for (int t = warp; t < NT; t += 8) {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) s += acc[t * 256 + r * 32 + lane];
+    for (int o2 = 16; o2; o2 >>= 1) s += __shfl_down_sync(0xffffffffu, s, o2);
+    if (lane == 0) partial[(slot * nchunks + chunk) * nterm_total + outs[t]] = s;
+  }
+}
+)";
+  return o.str();
+}
+
+std::string ev_jit_build(const std::vector<std::string>& srcs, std::vector<JitKernel>& out) {
+  out.assign(srcs.size(), JitKernel());
+  if (!jit_available()) return "libnvrtc not available";
+  const std::string dir = cache_dir();
+  std::vector<JitJob> jobs(srcs.size());
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    JitJob& j = jobs[i];
+    j.pass = (int)i;
+    j.src = srcs[i];
+    std::string key = j.src;
+    for (const char* opt : kOpts) key += opt;
+    key += "nvrtc " + std::to_string(nvrtc().major) + "." + std::to_string(nvrtc().minor);
+    char name[64];
+    snprintf(name, sizeof(name), "/ev%016llx.cubin", (unsigned long long)fnv1a(key));
+    j.path = dir + name;
+    std::ifstream f(j.path, std::ios::binary);
+    if (f) {
+      j.cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+      j.ok = j.from_cache = !j.cubin.empty();
+    }
+  }
+  std::atomic<size_t> next(0);
+  unsigned nthreads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+  std::vector<std::thread> pool;
+  for (unsigned w = 0; w < nthreads; ++w)
+    pool.emplace_back([&] {
+      for (size_t i = next++; i < jobs.size(); i = next++) {
+        JitJob& j = jobs[i];
+        if (j.ok) continue;
+        j.ok = compile_one(j.src, j.cubin, j.log);
+        if (j.ok) write_cache(j.path, j.cubin);
+      }
+    });
+  for (auto& th : pool) th.join();
+  std::string err;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    JitJob& j = jobs[i];
+    if (!j.ok) {
+      err = "NVRTC failed for reducer kernel: " + j.log.substr(0, 2000);
+      continue;
+    }
+    cudaLibrary_t lib;
+    if (cudaLibraryLoadData(&lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+      cudaGetLastError();
+      unlink(j.path.c_str());
+      err = "cudaLibraryLoadData failed for a reducer kernel";
+      continue;
+    }
+    cudaKernel_t k;
+    if (cudaLibraryGetKernel(&k, lib, "qsb_ev_jit") != cudaSuccess) {
+      cudaGetLastError();
+      cudaLibraryUnload(lib);
+      err = "cudaLibraryGetKernel failed for a reducer kernel";
+      continue;
+    }
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    out[i].lib = (void*)lib;
+    out[i].kern = (void*)k;
+  }
+  return err;
+}
+
 cudaError_t jit_launch(const JitKernel& jk, const StreamArgs& a, const PassDesc& pd, cudaStream_t s) {
   StreamArgs aa = a;
   PassDesc pp = pd;

@@ -58,6 +58,27 @@ std::string jit_compile_only(const TapeInfo& t, const StreamPlan& P, int c64, bo
 std::string jit_source(const TapeInfo& t, const StreamPlan& P, int pass, int c64, bool fuse);
 
 cudaError_t jit_launch(const JitKernel& jk, const StreamArgs& a, const PassDesc& pd, cudaStream_t s);
+
+// ---- NVRTC-specialised Pauli reducer (one launch group of k_expval_acc) ---------------
+struct EvJitMap {
+  int tpos[8];         // thread bit i -> tile position
+  uint16_t soff[16];   // swizzled slot offset of register j
+  int t0, nt;          // its terms [t0, t0 + nt) (launch-relative)
+};
+struct EvJitTerm {
+  uint32_t xr, zsig, zl;
+  uint64_t zg;
+  int ny, out;
+};
+struct EvJitSpec {
+  int c64 = 0, lowq = 2;
+  std::vector<EvJitMap> maps;
+  std::vector<EvJitTerm> terms;  // sorted by (map, xr, Re/Im) like the generic launch
+};
+std::string ev_jit_source(const EvJitSpec& s);
+// compile (parallel, disk-cached) and load one kernel per source; out[i] receives the kernel
+// of srcs[i] (kern == nullptr on failure, then the caller runs the generic kernel)
+std::string ev_jit_build(const std::vector<std::string>& srcs, std::vector<JitKernel>& out);
 void jit_release(std::vector<JitKernel>& ks);
 
 }  // namespace qsb
