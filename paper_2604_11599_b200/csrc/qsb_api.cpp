@@ -963,7 +963,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
         const ExpvalTerm& e = dev_terms[g.term_begin + t];
         sp.terms.push_back(EvJitTerm{e.xr, e.zsig, e.zl, e.zg, e.ny, e.out});
       }
-      srcs[gi] = ev_jit_source(sp) + "// smask " + std::to_string(g.smask) + "\n";
+      srcs[gi] = ev_jit_source(sp);  // smask is a kernel argument: one kernel per structure
       keys[gi] = std::hash<std::string>()(srcs[gi]);
       auto it = ctx->ev_jit.find(keys[gi]);
       if (it != ctx->ev_jit.end()) jk[gi] = it->second.second;
