@@ -510,10 +510,11 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
-  else if (k == "jit_async") ctx->opt_jit_async = value;
+  else if (k == "jit_async") ctx->opt_jit_async = value;  // NVRTC in the background, generic kernel meanwhile
   else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles
-  else if (k == "expval_jit") ctx->opt_ev_jit = value;  // NVRTC-specialised Pauli reducer  // NVRTC in the background, generic kernel meanwhile
-  else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (4 complex128, 5 complex64)
+  else if (k == "expval_jit") ctx->opt_ev_jit = value;          // NVRTC-specialised Pauli reducer
+  else if (k == "expval_jit_terms") ctx->opt_ev_jit_terms = value;  // its terms per launch (<= 32)
+  else if (k == "low_qubits") ctx->opt_lowq = value;   // 0: default (3)
   else if (k == "reg_bits") {                       // register-blocked phases: 3..5 register qubits
     if (value < 3 || value > 5) return fail(QSB_ERR_ARG, "reg_bits must be 3, 4 or 5");
     ctx->opt_reg_bits = value;
@@ -759,6 +760,10 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   std::vector<ExpvalGroup> dev_groups;  // pair-loop launches (path 1)
   std::vector<ExpvalGroup> acc_groups;  // accumulating launches (path 0, k = 12)
   std::vector<EvClass> dev_classes;
+  // NVRTC-specialised reducer for observe-sized jobs: register accumulators allow larger
+  // launches (fewer reads of the states); the generic kernel keeps kEvAccTerms
+  const bool use_ev_jit = ctx->opt_jit && ctx->opt_ev_jit && n >= 16 && nterm >= 8 && jit_available();
+  const int ev_jit_terms = use_ev_jit ? (int)std::max<int64_t>(1, std::min<int64_t>(32, ctx->opt_ev_jit_terms)) : kEvAccTerms;
   std::vector<EvMap> dev_maps;
   const int sb = c64 ? 4 : 3;
   for (Grp& g : groups) {
@@ -812,6 +817,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
       // of equal patterns is one run (its pair products are formed once), then cut into
       // launches of <= kEvAccTerms terms (the per-thread accumulators of one launch live
       // in shared memory: kEvAccTerms x 256 doubles)
+      const int cap = ev_jit_terms;
       auto flush_launch = [&](ExpvalGroup& cur) {
         if (cur.nterm) {  // its classes: runs of equal xr per mapping part (Re before Im)
           cur.cls_begin = (int)dev_classes.size();
@@ -869,8 +875,8 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
         });
         size_t i = 0;
         while (i < mts.size()) {
-          if (cur.nterm == kEvAccTerms) flush_launch(cur);
-          const size_t take = std::min<size_t>(mts.size() - i, (size_t)(kEvAccTerms - cur.nterm));
+          if (cur.nterm == cap) flush_launch(cur);
+          const size_t take = std::min<size_t>(mts.size() - i, (size_t)(cap - cur.nterm));
           EvMap part = em;
           part.term_begin = (int)dev_terms.size();
           part.nterm = (int)take;
@@ -941,7 +947,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
   // NVRTC-specialised reducer per launch group (observe-sized jobs; compiled once per
   // Hamiltonian grouping and cached per context and on disk), else the generic kernel
   std::vector<void*> jk(acc_groups.size(), nullptr);
-  if (ctx->opt_jit && ctx->opt_ev_jit && n >= 16 && nterm >= 8 && !acc_groups.empty() && jit_available()) {
+  if (use_ev_jit && !acc_groups.empty()) {
     std::vector<std::string> srcs(acc_groups.size());
     std::vector<size_t> keys(acc_groups.size());
     std::vector<size_t> missing;
@@ -989,7 +995,7 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
     }
     const size_t amp = c64 ? 8 : 16;
     auto up = [](size_t b) { return (b + 15) & ~(size_t)15; };
-    const size_t smem = up((c64 ? 2 : 1) * amp * 4096) + up(sizeof(double) * 256 * (size_t)g.nterm) +
+    const size_t smem = up((c64 ? 2 : 1) * amp * 4096) +
                         up(sizeof(uint64_t) * (4096 >> lowq)) + up(sizeof(uint32_t) * (4096 >> (c64 ? 4 : 3))) +
                         up(sizeof(uint64_t) * 32) + up(sizeof(uint32_t) * 2) + 16;
     const int nchunks_i = nchunks;

@@ -871,12 +871,12 @@ std::string ev_jit_source(const EvJitSpec& S) {
   o << "extern \"C\" __global__ void __launch_bounds__(256, 2) qsb_ev_jit(const A* __restrict__ states, int n, "
        "unsigned long long smask, double* __restrict__ partial, int nterm_total, int nchunks) {\n";
   o << "  constexpr int SB = " << sbits << ", K = 12, TL = 4096, LOWQ = " << S.lowq << ", NT = " << T
-    << ", NBUF = " << nbuf << ", TPC_MAX = 32;\n";
+    << ", NBUF = " << nbuf << ", TPC_MAX = 32;\n  constexpr bool REGACC = " << (S.regacc ? "true" : "false") << ";\n";
   o << R"(  extern __shared__ __align__(16) unsigned char smem_raw[];
   size_t off = 0;
   auto carve = [&](size_t bytes) { unsigned char* p = smem_raw + off; off = (off + bytes + 15) & ~(size_t)15; return p; };
   A* tiles = reinterpret_cast<A*>(carve(sizeof(A) * NBUF * TL));
-  double* acc = reinterpret_cast<double*>(carve(sizeof(double) * NT * 256));
+  double* acc = reinterpret_cast<double*>(carve(sizeof(double) * (REGACC ? 0 : NT) * 256));
   uint64_t* hi_off = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * (TL >> LOWQ)));
   uint32_t* swz = reinterpret_cast<uint32_t*>(carve(sizeof(uint32_t) * (TL >> SB)));
   uint64_t* ibase = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * TPC_MAX));
@@ -895,9 +895,11 @@ std::string ev_jit_source(const EvJitSpec& S) {
   }
   const uint64_t outmask = ~smask & qmask;
   for (int i = tid; i < TPC_MAX; i += 256) ibase[i] = qsb::pdep64((uint64_t)i, outmask);
-  for (int i = tid; i < NT * 256; i += 256) acc[i] = 0.0;
+  for (int i = tid; i < (REGACC ? 0 : NT) * 256; i += 256) acc[i] = 0.0;
   __syncthreads();
 )";
+  if (S.regacc)
+    for (int t = 0; t < T; ++t) o << "  double acc" << t << " = 0.0;\n";
   // per-thread parity word: bit t = parity(thread's tile bits of t's mapping & zl_t) = parity(tid & TM_t)
   o << "  const uint32_t pthread = 0u";
   for (const EvJitMap& m : S.maps)
@@ -947,7 +949,10 @@ std::string ev_jit_source(const EvJitSpec& S) {
     const uint32_t pw = pthread ^ tword[i & 1];
 )";
   auto acc_line = [&](int t, const std::string& s) {
-    o << "      acc[" << t << " * 256 + tid] += sgnd((double)(" << s << "), (pw << " << (31 - t) << ") & 0x80000000u);\n";
+    if (S.regacc)
+      o << "      acc" << t << " += sgnd((double)(" << s << "), (pw << " << (31 - t) << ") & 0x80000000u);\n";
+    else
+      o << "      acc[" << t << " * 256 + tid] += sgnd((double)(" << s << "), (pw << " << (31 - t) << ") & 0x80000000u);\n";
   };
   for (size_t mi = 0; mi < S.maps.size(); ++mi) {
     const EvJitMap& m = S.maps[mi];
@@ -1017,6 +1022,11 @@ std::string ev_jit_source(const EvJitSpec& S) {
     if (NBUF == 1 && i + 1 < tpc) load(i + 1, tiles);
   }
 )";
+  if (S.regacc) {  // the register accumulators -> shared memory (the tile buffer is free now)
+    o << "  double* red = reinterpret_cast<double*>(tiles);\n";
+    for (int t = 0; t < T; ++t) o << "  red[" << t << " * 256 + tid] = acc" << t << ";\n";
+    o << "  __syncthreads();\n  acc = red;\n";
+  }
   o << "  const int outs[" << std::max(1, T) << "] = {";
   for (int t = 0; t < T; ++t) o << (t ? ", " : "") << S.terms[t].out;
   if (!T) o << "0";

@@ -72,6 +72,7 @@ struct EvJitTerm {
 };
 struct EvJitSpec {
   int c64 = 0, lowq = 2;
+  bool regacc = true;            // per-term accumulators in registers (else shared memory)
   std::vector<EvJitMap> maps;
   std::vector<EvJitTerm> terms;  // sorted by (map, xr, Re/Im) like the generic launch
 };
