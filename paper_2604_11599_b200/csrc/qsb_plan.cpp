@@ -51,27 +51,45 @@ uint32_t swizzle_hi(uint32_t hi, int sb) {
 static uint32_t swz_slot(uint32_t l, int sb) { return l ^ swizzle_hi(l >> sb, sb); }
 static uint32_t swz_vec(int p, int sb) { return p < sb ? (1u << p) : (sb == 3 ? kV3[p] : kV4[p]); }
 
-void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff) {
+void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff, uint32_t avoid) {
   uint32_t R = 0;
   for (int b = 0; b < rb; ++b) R |= 1u << rpos[b];
   // thread positions: first sb positions with independent swizzle vectors, so that
-  // 2^sb consecutive threads hit distinct bank groups
+  // 2^sb consecutive threads (the lanes one shared-memory wavefront serves: 8 for 16-byte,
+  // 16 for 8-byte amplitudes) hit distinct bank groups.  Positions in `avoid` (thread
+  // controls of the phase's X gates, which the generator folds into a per-thread XOR of
+  // the slot: an XOR that differs inside a wavefront's lanes would break the distinctness)
+  // are taken for those first sb slots only when nothing else is independent.
   std::vector<int> tp, others;
   uint32_t basis[8] = {0};
-  for (int p = 0; p < k; ++p) {
-    if (R >> p & 1) continue;
-    uint32_t v = swz_vec(p, sb);
+  auto reduce = [&](uint32_t v) {
     for (int b = sb - 1; b >= 0 && v; --b)
       if (v >> b & 1) {
         if (basis[b]) v ^= basis[b];
-        else {
-          basis[b] = v;
-          break;
-        }
+        else return v;
       }
-    if (v && (int)tp.size() < sb) tp.push_back(p);
-    else others.push_back(p);
-  }
+    return v;
+  };
+  auto insert = [&](uint32_t v) {
+    for (int b = sb - 1; b >= 0; --b)
+      if (v >> b & 1) {
+        basis[b] = v;
+        return;
+      }
+  };
+  std::vector<char> used(k, 0);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int p = 0; p < k && (int)tp.size() < sb; ++p) {
+      if ((R >> p & 1) || used[p] || ((avoid >> p & 1) && pass == 0)) continue;
+      const uint32_t v = reduce(swz_vec(p, sb));
+      if (v) {
+        insert(v);
+        tp.push_back(p);
+        used[p] = 1;
+      }
+    }
+  for (int p = 0; p < k; ++p)
+    if (!(R >> p & 1) && !used[p]) others.push_back(p);
   for (int p : others) tp.push_back(p);
   for (int i = 0; i < k - rb; ++i) tpos[i] = (int8_t)tp[i];
   for (int j = 0; j < (1 << rb); ++j) {
@@ -400,7 +418,12 @@ struct Planner {
           rj[p] = nr++;
         }
       }
-      tile_mapping(rpos, rb, k, sb, ph.tpos, ph.soff);
+      uint32_t avoid = 0;  // thread-position controls of X gates (edge-X slot flips)
+      for (int gi : take) {
+        const PassGate& g = P.gates[gi];
+        if (g.gclass == GC_XPERM) avoid |= g.lcm & ~R;
+      }
+      tile_mapping(rpos, rb, k, sb, ph.tpos, ph.soff, avoid);
       ph.gate_begin = (int)P.phase_gates.size();
       for (int gi : take) {
         const PassGate& g = P.gates[gi];

@@ -34,7 +34,7 @@ uint32_t swizzle_hi(uint32_t hi, int sb);  // V applied to tile bits >= sb (hi =
 // register / thread mapping of a swizzled k-position tile: register bit b <-> tile
 // position rpos[b] (b < rb); writes the k - rb thread positions and the swizzled slot
 // offset of each of the 2^rb registers
-void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff);
+void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t* soff, uint32_t avoid = 0);
 
 // Engine options of the planner and the NVRTC generator, set per context
 // (qsb_ctx_set_option); the defaults are the settings measured best on B200 (DESIGN.md
