@@ -229,10 +229,10 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     cb = cpu_baseline(args.steps, args.warmup)
-    cfg = base_config(args.batch, args.gpus, args.precision)
-    cfg["engine"] = "CPU: " + ("reference qasm2cudaq sim (baseline/_ref)" if cb["kind"] == "reference"
-                               else "oracle port of the reference sim")
+    cfg = base_config(args.batch, args.gpus, args.precision)  # identical keys and values to our arm's
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "shots/s",
+            "engine": "CPU: " + ("reference qasm2cudaq sim (baseline/_ref)" if cb["kind"] == "reference"
+                                 else "oracle port of the reference sim"),
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": cfg,
@@ -358,7 +358,8 @@ def run_ours(args) -> None:
             "vs_baseline": None,
             "dtype": "f64" if prec == "c128" else "f32",
             "data": "synthetic",
-            "config": {**base_config(B, world, prec), "engine": "streaming (fused passes + decide)"},
+            "config": base_config(B, world, prec),
+            "engine": "streaming (fused passes + decide)",
             "tile_qubits": ctx.stats()["tile_qubits"],
             "comm": comm,
             "gate_updates_per_s": gate_updates_all / (dev_ms_max / 1000.0),
