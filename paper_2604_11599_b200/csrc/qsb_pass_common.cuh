@@ -17,10 +17,13 @@ __constant__ uint8_t c_swz3[16] = {1, 2, 4, 3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7, 1, 
 __constant__ uint8_t c_swz4[16] = {1, 2, 4, 8, 3, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 1};
 
 // a pass gate staged in shared memory with its CTA-uniform decisions resolved
+// 112 B (complex128) / 80 B (complex64): strides of 28 / 20 banks, so the 16-byte stores
+// of 8 consecutive staging threads hit distinct bank groups (96 / 64 B were 2- / 4-way)
 template <typename R> struct SGate {
   int32_t kind, jt, jt2, tp;
   uint32_t cmR, cvR, cmT, cvT;
   R m[8];
+  int32_t pad[4];
 };
 
 __device__ __forceinline__ uint64_t pext64(uint64_t v, uint64_t mask) {
@@ -189,7 +192,7 @@ __host__ __device__ inline int pass_groups(int mode) { return 1; }
 __host__ __device__ inline size_t pass_reg_smem(int c64, const PassDesc& pd, int rb, int n, bool stage, int mode = 0) {
   const int sb = c64 ? 4 : 3;
   const size_t amp = c64 ? 8 : 16;
-  const size_t sgate = c64 ? 64 : 96;
+  const size_t sgate = c64 ? 80 : 112;  // sizeof(SGate<float / double>)
   const int G = pass_groups(mode);
   return pass_buffers(c64, mode) * (amp << pd.k) + G * (stage ? sgate * pd.pgate_count : 0) +
          (sizeof(uint64_t) << (pd.k - pd.lowq)) + (sizeof(uint32_t) << (pd.k - sb)) +
