@@ -23,5 +23,5 @@ for spec in ["base"] + sys.argv[1:]:
     print(json.dumps(out), flush=True)
     if spec != "base":
         from importlib import reload
-        ctx.set_option(key, {"phase_search": 0, "pair_aware": 1, "minblocks": 2, "inline_phases": -1,
+        ctx.set_option(key, {"phase_search": 1, "pair_aware": 1, "minblocks": 2, "inline_phases": -1,
                              "edge_x": 1, "last_direct": 1, "fuse": 1}.get(key, 0))

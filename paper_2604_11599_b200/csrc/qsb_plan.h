@@ -41,7 +41,7 @@ void tile_mapping(const int* rpos, int rb, int k, int sb, int8_t* tpos, uint16_t
 // §7b).  Part of the plan cache key.
 struct EngineOptions {
   int pair_aware = 1;         // phase register sets follow two-qubit partners
-  int phase_search = 0;       // per-phase register-set search
+  int phase_search = 1;       // per-phase register-set search (round 2: measured faster on every config)
   int block_condx = 0;        // a conditional X ends its target's use in a phase
   int inline_phases = -1;     // phases inlined into the pass kernel (-1: complex128 yes, complex64 no)
   int inline_min_gates = 0;   // ... only for passes with at least this many gates
