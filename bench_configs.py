@@ -111,8 +111,9 @@ def cfg4(args):
 
 def cfg5(args):
     """Sliced execution emulated on one GPU (8 slices = the 8 ranks of cfg 5): the whole
-    trajectory enqueued with device-side decisions; exchange counts of the look-ahead
-    planner vs the round-1 fixed-eviction rule, and the slice exchange rate on HBM."""
+    trajectory enqueued with device-side decisions; exchange counts and bytes of the
+    round-1 fixed-eviction rule, the look-ahead planner with pairwise exchanges, and the
+    look-ahead planner with grouped remaps of up to 3 positions."""
     import torch
 
     from paper_2604_11599_b200 import ir, sim, sliced, workloads
@@ -120,8 +121,8 @@ def cfg5(args):
     for n, depth, fuse in ((args.sliced_qubits, 40, None), (30, 20, True)):
         _, k = workloads.rdc_circuit(n=n, depth=depth, every=20 if depth == 40 else 10, seed=34)
         b = ir.bind(k, [])
-        for la in (False, True):
-            plan = sliced.plan_slices(k, b.values, 3, lookahead=la)
+        for la, group in ((False, 1), (True, 1), (True, 3)):
+            plan = sliced.plan_slices(k, b.values, 3, lookahead=la, group=group)
             best = None
             for rep in range(2):  # the first run pays slice allocation
                 torch.cuda.synchronize()
@@ -132,10 +133,13 @@ def cfg5(args):
                 dt = time.perf_counter() - t0
                 best = dt if best is None else min(best, dt)
                 del st
+            how = "fixed top-position eviction" if not la else (
+                "look-ahead eviction, pairwise exchanges" if group == 1 else "look-ahead eviction, grouped remaps")
             _emit({"config": f"cfg5 sliced RDC{n} depth {depth}, 3 global qubits emulated on 1 GPU (8 slices of "
-                             f"2^{n - 3}), {'look-ahead' if la else 'fixed top-position'} eviction",
+                             f"2^{n - 3}), {how}",
                    "trajectory_s": best, "exchanges": plan.exchanges, "key": store.key(),
-                   "exchange_bytes_per_gpu": plan.exchanges * (16 << (n - 4))})
+                   "remap_sizes": sorted({len(s[1]) for s in plan.steps if s[0] == "xchg"}),
+                   "exchange_bytes_per_gpu": int(plan.volume * (16 << (n - 3)))})
 
 
 def cfg5_single(args):

@@ -283,6 +283,14 @@ int32_t qsb_slice_collapse(qsb_state st, qsb_slicectl c, int32_t qubit, int32_t 
 /* single device: swap global position <-> local position pos between the slice pair
  * (a: global bit 0, b: global bit 1) in place                                         */
 int32_t qsb_slice_exchange_local(qsb_state a, qsb_state b, int32_t pos);
+/* single device: remap k = 1..3 global positions with local positions lpos[0..k) across
+ * the 2^k slices group[0 .. 2^k) (group[y]: remapped global bits y) -- the amplitude at
+ * (slice y, local bits x at lpos) moves to (slice x, local bits y), in place            */
+int32_t qsb_slice_remap_local(const qsb_state* group, int32_t k, const int32_t* lpos);
+/* host copy of / into the region of a slice whose local bits at lpos equal x (2^(n-k)
+ * amplitudes in the slice's precision, increasing order of the other bits)             */
+int32_t qsb_slice_read_sub(qsb_state st, int32_t k, const int32_t* lpos, int32_t x, void* host_out);
+int32_t qsb_slice_write_sub(qsb_state st, int32_t k, const int32_t* lpos, int32_t x, const void* host_in);
 
 /* NCCL data plane (libnccl.so.2 opened at run time; QSB_ERR_UNSUPPORTED without it)    */
 int32_t qsb_comm_unique_id(uint8_t* out128);                  /* rank 0, broadcast by the caller */
@@ -296,6 +304,10 @@ int32_t qsb_comm_allgather_partials(qsb_comm c, qsb_slicectl s);
  * ncclRecv on the context stream.  Production: send == recv (in place).               */
 int32_t qsb_comm_exchange(qsb_comm c, qsb_state send, int32_t send_c, qsb_state recv, int32_t recv_c, int32_t pos,
                           int32_t peer);
+/* remap of k = 1..3 global positions among the ranks peers[0 .. 2^k) (this rank =
+ * peers[self]): region x of this slice goes to peers[x], peers[x]'s region `self` comes
+ * back into region x -- grouped ncclSend / ncclRecv to all 2^k - 1 peers per chunk      */
+int32_t qsb_comm_remap(qsb_comm c, qsb_state st, int32_t k, const int32_t* lpos, const int32_t* peers, int32_t self);
 /* out3 = {bytes sent, exchanges, all-gathers}; CUDA-event ms of the last exchange     */
 int32_t qsb_comm_stats(qsb_comm c, int64_t* out3, double* last_exchange_ms);
 int32_t qsb_comm_nccl_version(int32_t* version);

@@ -129,12 +129,16 @@ _SIGS = {
     "qsb_slice_decide": (_I32, [_P, _I32, _I32]),
     "qsb_slice_collapse": (_I32, [_P, _P, _I32, _I32, _I32]),
     "qsb_slice_exchange_local": (_I32, [_P, _P, _I32]),
+    "qsb_slice_remap_local": (_I32, [_P, _I32, _P]),
+    "qsb_slice_read_sub": (_I32, [_P, _I32, _P, _I32, _P]),
+    "qsb_slice_write_sub": (_I32, [_P, _I32, _P, _I32, _P]),
     "qsb_comm_unique_id": (_I32, [_P]),
     "qsb_comm_init": (_I32, [_P, _P, _I32, _I32, ctypes.POINTER(_P)]),
     "qsb_comm_destroy": (_I32, [_P]),
     "qsb_comm_set_chunk": (_I32, [_P, _I64]),
     "qsb_comm_allgather_partials": (_I32, [_P, _P]),
     "qsb_comm_exchange": (_I32, [_P, _P, _I32, _P, _I32, _I32, _I32]),
+    "qsb_comm_remap": (_I32, [_P, _P, _I32, _P, _P, _I32]),
     "qsb_comm_stats": (_I32, [_P, _P, _PD]),
     "qsb_comm_nccl_version": (_I32, [ctypes.POINTER(_I32)]),
 }

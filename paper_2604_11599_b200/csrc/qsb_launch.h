@@ -156,6 +156,11 @@ void launch_slice_put(const double* blocks, int nblocks, int select, double* par
 void launch_slice_decide(SliceCtl* c, const double* partials, int nslices, int kind, int bit, cudaStream_t s);
 void launch_slice_collapse(int c64, void* amps, int n, int q, int gbit, int flip, const SliceCtl* ctl,
                            cudaStream_t s);
+void launch_slice_remap_local(int c64, void* const* group, int n, int k, const int* lpos, cudaStream_t s);
+void launch_slice_pack_sub(int c64, const void* amps, int k, const int* lpos, int x, int64_t first, int64_t count,
+                           void* out, cudaStream_t s);
+void launch_slice_unpack_sub(int c64, void* amps, int k, const int* lpos, int x, int64_t first, int64_t count,
+                             const void* in, cudaStream_t s);
 void launch_slice_exchange_local(int c64, void* a, void* b, int n, int pos, cudaStream_t s);
 void launch_slice_pack(int c64, const void* amps, int pos, int c, int64_t first, int64_t count, void* out,
                        cudaStream_t s);

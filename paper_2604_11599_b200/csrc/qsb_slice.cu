@@ -15,8 +15,13 @@
 //   * a swap of a global position with local position `pos` moves the amplitudes whose
 //     local bit `pos` differs from the slice's global bit to the partner slice: in place
 //     on one device (k_slice_exchange_local), or packed / NCCL send-recv / unpacked in
-//     chunks across ranks (k_slice_pack / k_slice_unpack, qsb_slice_api.cpp).
+//     chunks across ranks (k_slice_pack / k_slice_unpack, qsb_slice_api.cpp);
+//   * a remap of k = 2..3 global positions at once is a transpose of 2^k x 2^k blocks
+//     across a group of 2^k slices (k_slice_remap_local on one device; k_slice_pack_sub /
+//     grouped NCCL send-recv to the 2^k - 1 peers / k_slice_unpack_sub across ranks).
 #include <cuda_runtime.h>
+
+#include <utility>
 
 #include "qsb_device.cuh"
 #include "qsb_launch.h"
@@ -198,7 +203,107 @@ __global__ void __launch_bounds__(kST) k_slice_unpack(typename Amp<R>::T* amps, 
     amps[insert_zero((uint64_t)(first + k), pos) | set] = in[k];
 }
 
+// k-position remaps (1 <= k <= 3).  A group of 2^k slices differing only in the k global
+// bits being swapped is indexed by y (bit i <-> global position i of the remap); local
+// positions lpos[i] pair with them.  Swapping global position i with lpos[i] for all i at
+// once moves the amplitude at (slice y, local bits x at lpos, rest r) to (slice x, local
+// bits y, rest r): a transpose of the 2^k x 2^k blocks, one per r.
+struct RemapArg {
+  int k;
+  int lpos[3];   // pairing order
+  int sorted[3]; // ascending (zero insertion)
+};
+
+__device__ __forceinline__ uint64_t remap_base(uint64_t r, const RemapArg& a) {
+  for (int i = 0; i < a.k; ++i) r = insert_zero(r, a.sorted[i]);
+  return r;
+}
+
+__device__ __forceinline__ uint64_t remap_spread(int x, const RemapArg& a) {
+  uint64_t v = 0;
+  for (int i = 0; i < a.k; ++i) v |= (uint64_t)((x >> i) & 1) << a.lpos[i];
+  return v;
+}
+
+template <typename R>
+struct GroupPtrs {
+  typename Amp<R>::T* p[8];
+};
+
+// in place on one device: every off-diagonal pair (x < y) of every block swapped once
+template <typename R>
+__global__ void __launch_bounds__(kST) k_slice_remap_local(GroupPtrs<R> g, int n, RemapArg a) {
+  const int64_t rows = 1ll << (n - a.k);
+  const int m = 1 << a.k;
+  for (int64_t r = blockIdx.x * (int64_t)kST + threadIdx.x; r < rows; r += (int64_t)gridDim.x * kST) {
+    const uint64_t base = remap_base((uint64_t)r, a);
+    for (int y = 1; y < m; ++y)
+      for (int x = 0; x < y; ++x) {
+        typename Amp<R>::T* py = g.p[y] + (base | remap_spread(x, a));
+        typename Amp<R>::T* px = g.p[x] + (base | remap_spread(y, a));
+        const auto t = *py;
+        *py = *px;
+        *px = t;
+      }
+  }
+}
+
+// the rows of one slice whose local bits at lpos equal x, in increasing order of the rest
+template <typename R>
+__global__ void __launch_bounds__(kST) k_slice_pack_sub(const typename Amp<R>::T* amps, RemapArg a, int x,
+                                                        int64_t first, int64_t count, typename Amp<R>::T* out) {
+  const uint64_t set = remap_spread(x, a);
+  for (int64_t j = blockIdx.x * (int64_t)kST + threadIdx.x; j < count; j += (int64_t)gridDim.x * kST)
+    out[j] = amps[remap_base((uint64_t)(first + j), a) | set];
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kST) k_slice_unpack_sub(typename Amp<R>::T* amps, RemapArg a, int x, int64_t first,
+                                                          int64_t count, const typename Amp<R>::T* in) {
+  const uint64_t set = remap_spread(x, a);
+  for (int64_t j = blockIdx.x * (int64_t)kST + threadIdx.x; j < count; j += (int64_t)gridDim.x * kST)
+    amps[remap_base((uint64_t)(first + j), a) | set] = in[j];
+}
+
+RemapArg remap_arg(int k, const int* lpos) {
+  RemapArg a{};
+  a.k = k;
+  for (int i = 0; i < k; ++i) a.lpos[i] = a.sorted[i] = lpos[i];
+  for (int i = 0; i < k; ++i)
+    for (int j = i + 1; j < k; ++j)
+      if (a.sorted[j] < a.sorted[i]) std::swap(a.sorted[i], a.sorted[j]);
+  return a;
+}
+
 }  // namespace
+
+void launch_slice_remap_local(int c64, void* const* group, int n, int k, const int* lpos, cudaStream_t s) {
+  const RemapArg a = remap_arg(k, lpos);
+  const int g = sgrid(1ll << (n - k));
+  if (c64) {
+    GroupPtrs<float> p{};
+    for (int i = 0; i < (1 << k); ++i) p.p[i] = (float2*)group[i];
+    k_slice_remap_local<float><<<g, kST, 0, s>>>(p, n, a);
+  } else {
+    GroupPtrs<double> p{};
+    for (int i = 0; i < (1 << k); ++i) p.p[i] = (double2*)group[i];
+    k_slice_remap_local<double><<<g, kST, 0, s>>>(p, n, a);
+  }
+}
+
+void launch_slice_pack_sub(int c64, const void* amps, int k, const int* lpos, int x, int64_t first, int64_t count,
+                           void* out, cudaStream_t s) {
+  const RemapArg a = remap_arg(k, lpos);
+  if (c64) k_slice_pack_sub<float><<<sgrid(count), kST, 0, s>>>((const float2*)amps, a, x, first, count, (float2*)out);
+  else k_slice_pack_sub<double><<<sgrid(count), kST, 0, s>>>((const double2*)amps, a, x, first, count, (double2*)out);
+}
+
+void launch_slice_unpack_sub(int c64, void* amps, int k, const int* lpos, int x, int64_t first, int64_t count,
+                             const void* in, cudaStream_t s) {
+  const RemapArg a = remap_arg(k, lpos);
+  if (c64) k_slice_unpack_sub<float><<<sgrid(count), kST, 0, s>>>((float2*)amps, a, x, first, count, (const float2*)in);
+  else k_slice_unpack_sub<double><<<sgrid(count), kST, 0, s>>>((double2*)amps, a, x, first, count, (const double2*)in);
+}
 
 void launch_slice_init(SliceCtl* c, uint64_t seed, int64_t shot, const uint64_t* rng_init, int nwords,
                        cudaStream_t s) {

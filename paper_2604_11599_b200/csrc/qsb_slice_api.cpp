@@ -231,6 +231,76 @@ int32_t qsb_slice_exchange_local(qsb_state a, qsb_state b, int32_t pos) {
   return QSB_OK;
 }
 
+namespace {
+int check_remap(qsb_state st, int k, const int32_t* lpos) {
+  if (k < 1 || k > 3 || !lpos) return fail(QSB_ERR_ARG, "remap of 1..3 positions expected");
+  for (int i = 0; i < k; ++i) {
+    if (lpos[i] < 0 || lpos[i] >= st->n) return fail(QSB_ERR_ARG, "local position out of range");
+    for (int j = 0; j < i; ++j)
+      if (lpos[j] == lpos[i]) return fail(QSB_ERR_ARG, "local positions must differ");
+  }
+  return QSB_OK;
+}
+}  // namespace
+
+// single device: remap k global positions with local positions lpos[0..k) across the
+// group of 2^k slices (group[y]: global bits y of the remapped positions)
+int32_t qsb_slice_remap_local(const qsb_state* group, int32_t k, const int32_t* lpos) {
+  if (!group || k < 1 || k > 3) return fail(QSB_ERR_ARG, "remap of 1..3 positions expected");
+  void* ptrs[8];
+  for (int i = 0; i < (1 << k); ++i) {
+    if (check_state(group[i])) return fail(QSB_ERR_ARG, "null state");
+    if (group[i]->n != group[0]->n || group[i]->c64 != group[0]->c64 || group[i]->ctx != group[0]->ctx)
+      return fail(QSB_ERR_DIMENSION, "slices differ");
+    for (int j = 0; j < i; ++j)
+      if (group[j] == group[i]) return fail(QSB_ERR_ARG, "slices of a group must differ");
+    ptrs[i] = group[i]->amps.p;
+  }
+  if (int rc = check_remap(group[0], k, lpos)) return rc;
+  if (group[0]->n < k) return fail(QSB_ERR_ARG, "slice too small");
+  int lp[3];
+  for (int i = 0; i < k; ++i) lp[i] = lpos[i];
+  DeviceGuard g(group[0]->ctx->device);
+  launch_slice_remap_local(group[0]->c64, ptrs, group[0]->n, k, lp, group[0]->ctx->stream);
+  QSB_CUDA(cudaGetLastError());
+  return QSB_OK;
+}
+
+// host staging of one remap region (local bits at lpos == x, increasing order of the
+// other bits; 2^(n-k) amplitudes in the slice's precision): the torch.distributed
+// transport and the tests
+int32_t qsb_slice_read_sub(qsb_state st, int32_t k, const int32_t* lpos, int32_t x, void* host_out) {
+  if (check_state(st) || !host_out) return fail(QSB_ERR_ARG, "null argument");
+  if (int rc = check_remap(st, k, lpos)) return rc;
+  if (x < 0 || x >= (1 << k)) return fail(QSB_ERR_ARG, "region index out of range");
+  DeviceGuard g(st->ctx->device);
+  const int64_t cnt = 1ll << (st->n - k), amp = st->c64 ? 8 : 16;
+  DevBuf tmp;
+  QSB_CUDA(tmp.ensure(cnt * amp));
+  int lp[3];
+  for (int i = 0; i < k; ++i) lp[i] = lpos[i];
+  launch_slice_pack_sub(st->c64, st->amps.p, k, lp, x, 0, cnt, tmp.p, st->ctx->stream);
+  QSB_CUDA(cudaMemcpyAsync(host_out, tmp.p, cnt * amp, cudaMemcpyDeviceToHost, st->ctx->stream));
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  return QSB_OK;
+}
+
+int32_t qsb_slice_write_sub(qsb_state st, int32_t k, const int32_t* lpos, int32_t x, const void* host_in) {
+  if (check_state(st) || !host_in) return fail(QSB_ERR_ARG, "null argument");
+  if (int rc = check_remap(st, k, lpos)) return rc;
+  if (x < 0 || x >= (1 << k)) return fail(QSB_ERR_ARG, "region index out of range");
+  DeviceGuard g(st->ctx->device);
+  const int64_t cnt = 1ll << (st->n - k), amp = st->c64 ? 8 : 16;
+  DevBuf tmp;
+  QSB_CUDA(tmp.ensure(cnt * amp));
+  int lp[3];
+  for (int i = 0; i < k; ++i) lp[i] = lpos[i];
+  QSB_CUDA(cudaMemcpyAsync(tmp.p, host_in, cnt * amp, cudaMemcpyHostToDevice, st->ctx->stream));
+  launch_slice_unpack_sub(st->c64, st->amps.p, k, lp, x, 0, cnt, tmp.p, st->ctx->stream);
+  QSB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  return QSB_OK;
+}
+
 // ---- NCCL data plane ----------------------------------------------------------------
 
 int32_t qsb_comm_unique_id(uint8_t* out128) {
@@ -323,6 +393,55 @@ int32_t qsb_comm_exchange(qsb_comm c, qsb_state send, int32_t send_c, qsb_state 
   cudaEventRecord(c->e1, s);
   QSB_CUDA(cudaGetLastError());
   c->bytes_sent += half * amp;
+  c->exchanges++;
+  return QSB_OK;
+}
+
+// A remap of k global positions (1..3) with local positions lpos[0..k) among the 2^k
+// ranks peers[0 .. 2^k) (peers[x]: the rank whose remapped global bits are x; this rank
+// is peers[self]).  For every x != self this rank sends its region x (local bits at lpos
+// == x) to peers[x] and receives peers[x]'s region `self` into its own region x: one
+// grouped ncclSend / ncclRecv round per chunk, all 2^k - 1 peers in flight at once, in
+// place (a chunk is packed before the same chunk is overwritten).  Moves (1 - 2^-k) of
+// the slice per rank where k separate pairwise exchanges move k / 2.
+int32_t qsb_comm_remap(qsb_comm c, qsb_state st, int32_t k, const int32_t* lpos, const int32_t* peers,
+                       int32_t self) {
+  if (!c || check_state(st) || !peers) return fail(QSB_ERR_ARG, "null argument");
+  if (int rc = check_remap(st, k, lpos)) return rc;
+  const int m = 1 << k;
+  if (self < 0 || self >= m || peers[self] != c->rank) return fail(QSB_ERR_ARG, "peers[self] must be this rank");
+  for (int x = 0; x < m; ++x)
+    if (peers[x] < 0 || peers[x] >= c->nranks) return fail(QSB_ERR_ARG, "peer out of range");
+  DeviceGuard g(c->ctx->device);
+  int lp[3];
+  for (int i = 0; i < k; ++i) lp[i] = lpos[i];
+  const int64_t amp = st->c64 ? 8 : 16;
+  const int64_t region = 1ll << (st->n - k);
+  const int64_t per = std::max<int64_t>(1, std::min<int64_t>(region, c->chunk_bytes / amp));
+  QSB_CUDA(c->sendbuf.ensure(per * amp * (m - 1)));
+  QSB_CUDA(c->recvbuf.ensure(per * amp * (m - 1)));
+  char* sb = (char*)c->sendbuf.p;
+  char* rb = (char*)c->recvbuf.p;
+  cudaStream_t s = c->ctx->stream;
+  cudaEventRecord(c->e0, s);
+  for (int64_t first = 0; first < region; first += per) {
+    const int64_t cnt = std::min(per, region - first);
+    for (int x = 0, j = 0; x < m; ++x)
+      if (x != self) launch_slice_pack_sub(st->c64, st->amps.p, k, lp, x, first, cnt, sb + (j++) * per * amp, s);
+    QSB_NCCL(nccl().group_start());
+    for (int x = 0, j = 0; x < m; ++x) {
+      if (x == self) continue;
+      QSB_NCCL(nccl().send(sb + j * per * amp, (size_t)(cnt * amp), ncclUint8, peers[x], c->comm, s));
+      QSB_NCCL(nccl().recv(rb + j * per * amp, (size_t)(cnt * amp), ncclUint8, peers[x], c->comm, s));
+      ++j;
+    }
+    QSB_NCCL(nccl().group_end());
+    for (int x = 0, j = 0; x < m; ++x)
+      if (x != self) launch_slice_unpack_sub(st->c64, st->amps.p, k, lp, x, first, cnt, rb + (j++) * per * amp, s);
+  }
+  cudaEventRecord(c->e1, s);
+  QSB_CUDA(cudaGetLastError());
+  c->bytes_sent += (int64_t)(m - 1) * region * amp;
   c->exchanges++;
   return QSB_OK;
 }

@@ -11,12 +11,15 @@ ENDIF, sim.py:296-301) and the data movement is decided once, before anything ru
 * a gate whose target is local runs on every slice (controls on global positions select
   slices, local controls go to the kernel); a diagonal gate on a global target is a
   per-slice phase;
-* a non-diagonal gate (or a reset) on a global position first EXCHANGES that global
-  position with a local one: the partner slices (s, s ^ bit) swap the halves in which the
-  local bit differs from their global bit (NCCL send/recv across GPUs, an in-place kernel
-  on one GPU).  The local position evicted is the one whose qubit is next needed locally
-  FARTHEST in the future (Belady look-ahead over the whole flattened program, branches
-  included) -- not a fixed position;
+* a non-diagonal gate (or a reset) on a global position first REMAPS that global
+  position with a local one -- together with every other global qubit needed locally
+  before the local qubit it would evict (up to G positions in one remap): within each
+  group of 2^k slices that differ only in the remapped global bits, the amplitude at
+  (slice y, local bits x) moves to (slice x, local bits y) -- grouped NCCL send/recv to
+  the 2^k - 1 peers across GPUs, an in-place kernel on one GPU; (1 - 2^-k) of a slice
+  per rank instead of k/2 for k pairwise exchanges.  The local positions evicted are the
+  ones whose qubits are next needed locally FARTHEST in the future (Belady look-ahead
+  over the whole flattened program, branches included) -- not a fixed position;
 * swap gates are relabelings of `perm` (no data movement).
 Because the plan does not depend on outcomes (a gate in an untaken branch still gets its
 exchange -- a relabeling that changes nothing logically), the host never has to wait for
@@ -58,7 +61,8 @@ class SlicePlan:
     n: int
     G: int
     steps: list = field(default_factory=list)  # see plan_slices
-    exchanges: int = 0
+    exchanges: int = 0    # remap steps
+    volume: float = 0.0   # slices sent per rank over all remaps (sum of 1 - 2^-k)
     final_perm: list = field(default_factory=list)
 
     @property
@@ -109,13 +113,18 @@ def _needs_local(item) -> int | None:
     return None
 
 
-def plan_slices(kernel, params, G: int, lookahead: bool = True) -> SlicePlan:
+def plan_slices(kernel, params, G: int, lookahead: bool = True, group: int | None = None) -> SlicePlan:
     """Static schedule of a sliced trajectory.  Steps (physical positions):
-        ("xchg", gpos, lpos)                         exchange a global with a local position
+        ("xchg", gposs, lposs)                       remap: global position gposs[i] <-> local
+                                                     position lposs[i], all at once
         ("gate", base, m, tpos, ctrls, guarded)      ctrls: ((pos, pol), ...)
         ("measure", pos, bit) / ("reset", pos)       reset positions are always local
         ("if", pred_record) / ("else",) / ("endif",)
-    `lookahead=False` evicts the top local position every time (the round-1 rule)."""
+    `lookahead=False` evicts the top local position every time (the round-1 rule).
+    `group` = most global positions one remap moves (default G): when a gate needs a
+    global qubit, every other global qubit that is needed locally BEFORE the local qubit
+    it would evict comes along in the same remap -- one all-to-all among 2^k ranks moves
+    (1 - 2^-k) of a slice per rank, against k/2 for k separate pairwise exchanges."""
     from . import _lib
     from .sim import _classical_offsets, _pred_record
 
@@ -123,6 +132,9 @@ def plan_slices(kernel, params, G: int, lookahead: bool = True) -> SlicePlan:
     if not 0 <= G < n:
         raise ValueError("need 0 <= G < n")
     L = n - G
+    kmax = G if group is None else max(1, min(int(group), G))
+    if not lookahead:
+        kmax = 1
     offsets = _classical_offsets([(nm, int(w)) for nm, w in kernel.classical_layout])
     items: list = []
     _flatten(kernel.body, items, offsets, params)
@@ -165,19 +177,29 @@ def plan_slices(kernel, params, G: int, lookahead: bool = True) -> SlicePlan:
             busy = set()
             if kind == "gate":
                 busy = {perm[c] for c, _ in it[4]}  # keep the gate's own controls local if possible
-            cands = [p for p in range(L)]
             if lookahead:
                 nxt = next_need[i + 1] if i + 1 < len(items) else [INF] * n
-                cands.sort(key=lambda p: (nxt[where[p]], p not in busy, p), reverse=True)
+                cands = sorted(range(L), key=lambda p: (nxt[where[p]], p not in busy, p), reverse=True)
+                # the other global qubits, soonest needed first, each paired with the next
+                # eviction candidate if it is needed before that candidate
+                others = sorted((nxt[where[g]], g) for g in range(L, n) if g != perm[q])
+                gposs, lposs = [perm[q]], [cands[0]]
+                for need, g in others:
+                    if len(gposs) >= kmax or need >= INF:
+                        break
+                    c = cands[len(lposs)]
+                    if need < nxt[where[c]]:
+                        gposs.append(g)
+                        lposs.append(c)
             else:
-                cands = [L - 1]
-            lpos = cands[0]
-            gpos = perm[q]
-            plan.steps.append(("xchg", gpos, lpos))
+                gposs, lposs = [perm[q]], [L - 1]
+            plan.steps.append(("xchg", tuple(gposs), tuple(lposs)))
             plan.exchanges += 1
-            ql = where[lpos]
-            perm[q], perm[ql] = lpos, gpos
-            where[lpos], where[gpos] = q, ql
+            plan.volume += 1.0 - 0.5 ** len(gposs)
+            for g, lp in zip(gposs, lposs):
+                qg, ql = where[g], where[lp]
+                perm[qg], perm[ql] = lp, g
+                where[lp], where[g] = qg, ql
         if kind == "gate":
             _, base, m, t, ctrls = it
             plan.steps.append(("gate", base, m, perm[t], tuple((perm[c], pol) for c, pol in ctrls), depth > 0))
@@ -312,6 +334,31 @@ class GpuSliceBackend:
         self.flush(b)
         self._lib().check(a._ctx.lib.qsb_slice_exchange_local(a._device(), b._device(), int(pos)))
 
+    def remap_local(self, group, lposs):
+        """Remap len(lposs) global positions across the 2^k slices `group` (index = the
+        remapped global bits) in one in-place kernel."""
+        for sl in group:
+            self.flush(sl)
+        _l = self._lib()
+        hs = (ctypes.c_void_p * len(group))(*[sl._device().value for sl in group])
+        lp = np.array(lposs, dtype=np.int32)
+        _l.check(group[0]._ctx.lib.qsb_slice_remap_local(hs, len(lposs), _l.ptr(lp)))
+
+    def pack_sub(self, st, lposs, x: int) -> np.ndarray:
+        self.flush(st)
+        _l = self._lib()
+        out = np.empty(1 << (st.n - len(lposs)), dtype=np.complex64 if st.precision == "c64" else np.complex128)
+        lp = np.array(lposs, dtype=np.int32)
+        _l.check(st._ctx.lib.qsb_slice_read_sub(st._device(), len(lposs), _l.ptr(lp), int(x), _l.ptr(out)))
+        return out
+
+    def unpack_sub(self, st, lposs, x: int, data) -> None:
+        self.flush(st)
+        _l = self._lib()
+        d = np.ascontiguousarray(data, dtype=np.complex64 if st.precision == "c64" else np.complex128)
+        lp = np.array(lposs, dtype=np.int32)
+        _l.check(st._ctx.lib.qsb_slice_write_sub(st._device(), len(lposs), _l.ptr(lp), int(x), _l.ptr(d)))
+
     def read_ctl(self, ctl, nwords: int):
         _l = self._lib()
         bits = np.zeros(max(1, nwords), dtype=np.uint64)
@@ -343,7 +390,8 @@ class _Ctl:
 
 class LocalTransport:
     """All slices in this process (single-device emulation of 2^G ranks): the partial
-    slots are already side by side, an exchange is an in-place kernel per slice pair."""
+    slots are already side by side, a remap is one in-place kernel per group of 2^k
+    slices."""
 
     def __init__(self, nslices: int):
         self.nslices = nslices
@@ -352,16 +400,17 @@ class LocalTransport:
     def allgather(self, backend, ctl) -> None:
         return None
 
-    def exchange(self, backend, slices, pairs, lpos):
-        for a, b in pairs:
-            backend.exchange_local(slices[a], slices[b], lpos)
+    def exchange(self, backend, slices, groups, lposs):
+        for g in groups:
+            backend.remap_local([slices[m] for m in g], lposs)
 
 
 class NcclTransport:
     """One slice per rank; the C-ABI NCCL communicator (qsb_comm_*) on the context's
-    stream: exchanges are chunked ncclSend/ncclRecv of the packed halves, the partials an
-    in-place ncclAllGather.  The unique id is broadcast over the default
-    torch.distributed group (the only host-side collective, once)."""
+    stream: a remap is chunked, grouped ncclSend/ncclRecv of the packed regions to the
+    2^k - 1 peers of this rank's group, the partials an in-place ncclAllGather.  The
+    unique id is broadcast over the default torch.distributed group (the only host-side
+    collective, once)."""
 
     def __init__(self, device=None, chunk_bytes: int | None = None):
         import torch.distributed as dist
@@ -388,17 +437,18 @@ class NcclTransport:
 
         _lib.check(self.ctx.lib.qsb_comm_allgather_partials(self.h, ctl.h))
 
-    def exchange(self, backend, slices, pairs, lpos):
+    def exchange(self, backend, slices, groups, lposs):
         from . import _lib
 
-        for a, b in pairs:
-            if self.rank not in (a, b):
+        for g in groups:
+            if self.rank not in g:
                 continue
             st = slices[self.rank]
             backend.flush(st)
-            c = 0 if self.rank == a else 1
-            peer = b if self.rank == a else a
-            _lib.check(self.ctx.lib.qsb_comm_exchange(self.h, st._device(), c, st._device(), c, int(lpos), peer))
+            peers = np.array(g, dtype=np.int32)
+            lp = np.array(lposs, dtype=np.int32)
+            _lib.check(self.ctx.lib.qsb_comm_remap(self.h, st._device(), len(lposs), _lib.ptr(lp), _lib.ptr(peers),
+                                                   g.index(self.rank)))
 
     def stats(self) -> dict:
         from . import _lib
@@ -418,7 +468,7 @@ class NcclTransport:
 class DistTransport:
     """One slice per rank over torch.distributed (the protocol of NcclTransport with
     host tensors: gloo in the CPU tests).  The backend provides `partials(ctl)` and
-    `pack` / `unpack` of a slice's exchanged half."""
+    `pack_sub` / `unpack_sub` of a slice's remap regions."""
 
     def __init__(self):
         import torch.distributed as dist
@@ -437,21 +487,27 @@ class DistTransport:
         for s in range(self.nslices):
             part[s] = float(out[s][0])
 
-    def exchange(self, backend, slices, pairs, lpos):
+    def exchange(self, backend, slices, groups, lposs):
         import torch
 
         dist = self.dist
-        for a, b in pairs:
-            if self.rank not in (a, b):
+        for g in groups:
+            if self.rank not in g:
                 continue
             st = slices[self.rank]
-            c = 0 if self.rank == a else 1
-            peer = b if self.rank == a else a
-            send = torch.from_numpy(backend.pack(st, lpos, c).view(np.float64).copy())
-            recv = torch.empty_like(send)
-            for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, peer), dist.P2POp(dist.irecv, recv, peer)]):
+            me = g.index(self.rank)
+            sends, recvs, ops = {}, {}, []
+            for x, peer in enumerate(g):
+                if x == me:
+                    continue
+                data = backend.pack_sub(st, lposs, x)
+                sends[x] = torch.from_numpy(np.ascontiguousarray(data).view(np.float64).copy())
+                recvs[x] = torch.empty_like(sends[x])
+                ops += [dist.P2POp(dist.isend, sends[x], peer), dist.P2POp(dist.irecv, recvs[x], peer)]
+            for r in dist.batch_isend_irecv(ops):
                 r.wait()
-            backend.unpack(st, lpos, c, recv.numpy().view(np.complex128))
+            for x, buf in recvs.items():
+                backend.unpack_sub(st, lposs, x, buf.numpy().view(np.complex128))
 
 
 # ---------------------------------------------------------------------------
@@ -526,10 +582,14 @@ def execute(plan: SlicePlan, st: SlicedState, ctl) -> None:
                 else:
                     be.collapse(sl, ctl, -1, st.gbit(s, p), False)
         elif kind == "xchg":
-            _, gpos, lpos = step
-            bit = 1 << (gpos - L)
-            pairs = [(s, s ^ bit) for s in range(1 << st.G) if not s & bit]
-            tr.exchange(be, st.slices, pairs, lpos)
+            _, gposs, lposs = step
+            bits = [1 << (g - L) for g in gposs]
+            mask = sum(bits)
+            # groups of 2^k slices that differ only in the remapped global bits, member
+            # y = the slice whose remapped bits are y
+            groups = [[s0 | sum(b for i, b in enumerate(bits) if y >> i & 1) for y in range(1 << len(bits))]
+                      for s0 in range(1 << st.G) if not s0 & mask]
+            tr.exchange(be, st.slices, groups, lposs)
             st.exchanges += 1
         elif kind == "if":
             be.guard(ctl, "if", step[1])
@@ -541,10 +601,11 @@ def execute(plan: SlicePlan, st: SlicedState, ctl) -> None:
 
 
 def run_trajectory_sliced(bound, rng, global_qubits: int, *, backend=None, transport=None, lookahead: bool = True,
-                          plan: SlicePlan | None = None):
+                          plan: SlicePlan | None = None, group: int | None = None):
     """run_trajectory (sim.py:306-314) on a state sliced over 2^global_qubits slices.
     `rng` must be an xoshiro stream (RngStream, ours or the reference's); it is advanced
-    by exactly the uniforms consumed.  Returns (ClassicalStore, SlicedState)."""
+    by exactly the uniforms consumed.  `group`: most global positions per remap (default
+    G; 1 = pairwise exchanges only).  Returns (ClassicalStore, SlicedState)."""
     from .sim import ClassicalStore, _rng_words
 
     k = bound.kernel
@@ -552,7 +613,7 @@ def run_trajectory_sliced(bound, rng, global_qubits: int, *, backend=None, trans
     backend = backend or GpuSliceBackend()
     transport = transport or LocalTransport(2**global_qubits)
     if plan is None:
-        plan = plan_slices(k, bound.values, global_qubits, lookahead=lookahead)
+        plan = plan_slices(k, bound.values, global_qubits, lookahead=lookahead, group=group)
     words = _rng_words(rng)
     if words is None:
         raise ValueError("the sliced engine draws on the device: pass an RngStream")

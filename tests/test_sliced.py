@@ -3,9 +3,12 @@
 * CPU: the sliced executor with a numpy slice backend (test-only stand-in for the
   device kernels) and the in-process transport -- exchanges, qubit relabeling, the
   global Pauli frame and slice-summed measurement give the oracle's trajectories.
-* CPU, gloo world size 2: one slice per rank, half-buffer exchanges over
-  torch.distributed send/recv, rank-ordered probability sums.
-* GPU: the product backend (C-ABI kernels) with the single-device transport.
+* CPU, gloo world size 2 / 4 / 8: one slice per rank, remaps of 1-3 positions as
+  packed region send/recv among each group of ranks over torch.distributed,
+  rank-ordered probability sums.
+* GPU: the product backend (C-ABI kernels) with the single-device transport, the remap
+  kernels against the numpy restatement, the NCCL data plane through a 1-rank
+  communicator.
 """
 
 import os
@@ -136,22 +139,27 @@ class NumpyBackend:
         else:
             a[i0] = keep
 
-    def exchange_local(self, a, b, pos):
+    def remap_local(self, group, lposs):
+        """(slice y, local bits x at lposs) -> (slice x, local bits y), in place."""
+        old = [a.copy() for a in group]
+        for y, a in enumerate(old):
+            for x in range(len(group)):
+                group[x][self._region(a, lposs, y)] = a[self._region(a, lposs, x)]
+
+    @staticmethod
+    def _spread(lposs, x):
+        return sum(((x >> i) & 1) << p for i, p in enumerate(lposs))
+
+    def _region(self, a, lposs, x):
         idx = np.arange(a.size)
-        i = idx[((idx >> pos) & 1) == 0]
-        x = a[i | (1 << pos)].copy()
-        a[i | (1 << pos)] = b[i]
-        b[i] = x
+        mask = self._spread(lposs, (1 << len(lposs)) - 1)
+        return idx[(idx & mask) == self._spread(lposs, x)]
 
-    def _region(self, a, pos, c):
-        idx = np.arange(a.size)
-        return idx[((idx >> pos) & 1) == (1 - c)]
+    def pack_sub(self, a, lposs, x):
+        return a[self._region(a, lposs, x)].copy()
 
-    def pack(self, a, pos, c):
-        return a[self._region(a, pos, c)].copy()
-
-    def unpack(self, a, pos, c, data):
-        a[self._region(a, pos, c)] = data
+    def unpack_sub(self, a, lposs, x, data):
+        a[self._region(a, lposs, x)] = data
 
     def partials(self, ctl):
         return ctl.partials
@@ -177,8 +185,8 @@ def _circuits():
     return out
 
 
-@pytest.mark.parametrize("G", [1, 2, 3])
-def test_sliced_numpy_matches_oracle(G):
+@pytest.mark.parametrize("G,group", [(1, None), (2, None), (3, None), (3, 1), (3, 2)])
+def test_sliced_numpy_matches_oracle(G, group):
     for k in _circuits():
         b = ir.bind(k, [])
         for shot in range(3):
@@ -189,7 +197,7 @@ def test_sliced_numpy_matches_oracle(G):
                 continue
             rng = sim.RngStream.for_shot(9, shot)
             store, st = sliced.run_trajectory_sliced(b, rng, G, backend=NumpyBackend(),
-                                                     transport=sliced.LocalTransport(2**G))
+                                                     transport=sliced.LocalTransport(2**G), group=group)
             assert store.key() == rs.key()
             assert rng.next_u64() == prng.next_u64()  # advanced by exactly the uniforms consumed
             np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-12)
@@ -226,10 +234,11 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(400)
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_sliced_gloo_ranks(world):
-    """One slice per rank (world 2: 1 global qubit, world 4: 2), exchanges as packed
-    send/recv, the partials all-gathered and summed in slice order on every rank."""
+    """One slice per rank (world 2: 1 global qubit, world 4: 2, world 8: 3), remaps of
+    up to G positions as packed send/recv to every peer of the rank's group, the
+    partials all-gathered and summed in slice order on every rank."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -260,22 +269,30 @@ def test_sliced_gloo_ranks(world):
 
 def test_lookahead_plan_fewer_exchanges():
     """Belady eviction (farthest next local use) against the round-1 rule (always the
-    top local position) on RDC26 depth 40 with 3 global qubits: fewer exchanges, same
-    trajectory (numpy backend, RDC10 twin)."""
+    top local position) on RDC26 depth 40 with 3 global qubits: fewer exchanges; grouped
+    remaps of up to 3 positions: fewer steps and < 80 % of the pairwise volume; the same
+    trajectory every way (numpy backend, RDC10 twin)."""
     _, k = workloads.rdc_circuit(n=26, depth=40, every=20, seed=30200)
     b = ir.bind(k, [])
     old = sliced.plan_slices(k, b.values, 3, lookahead=False).exchanges
-    new = sliced.plan_slices(k, b.values, 3, lookahead=True).exchanges
+    new = sliced.plan_slices(k, b.values, 3, lookahead=True, group=1).exchanges
     assert new < old, (new, old)
+    # grouped remaps (up to 3 positions per all-to-all): fewer steps and less volume
+    pair = sliced.plan_slices(k, b.values, 3, group=1)
+    grp = sliced.plan_slices(k, b.values, 3)
+    assert pair.exchanges == new and pair.volume == 0.5 * new
+    assert grp.exchanges < pair.exchanges and grp.volume < 0.8 * pair.volume, (grp.exchanges, grp.volume, pair.volume)
+    assert any(len(s[1]) == 3 for s in grp.steps if s[0] == "xchg")
     _, k = workloads.rdc_circuit(n=10, depth=40, every=20, seed=10)
     b = ir.bind(k, [])
     out = []
-    for la in (False, True):
+    for la, group in ((False, None), (True, 1), (True, None)):
         store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(5, 0), 3, backend=NumpyBackend(),
-                                                 transport=sliced.LocalTransport(8), lookahead=la)
+                                                 transport=sliced.LocalTransport(8), lookahead=la, group=group)
         out.append((store.key(), st.gather()))
-    assert out[0][0] == out[1][0]
-    np.testing.assert_allclose(out[0][1], out[1][1], atol=1e-12)
+    for key, amps in out[1:]:
+        assert key == out[0][0]
+        np.testing.assert_allclose(amps, out[0][1], atol=1e-12)
 
 
 @pytest.mark.gpu
@@ -407,3 +424,73 @@ def test_sliced_device_decisions_match_oracle_with_branches():
             assert store.key() == rs.key()
             np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-10)
             assert rng.next_u64() == prng.next_u64()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_remap_kernels_match_numpy(prec):
+    """qsb_slice_remap_local (k = 1, 2, 3; positions in pairing order, low and high) and
+    the region staging qsb_slice_read_sub / write_sub against the numpy restatement."""
+    from paper_2604_11599_b200.errors import BackendError
+
+    be, nb = sliced.GpuSliceBackend(precision=prec), NumpyBackend()
+    rng = np.random.default_rng(11)
+    L = 12
+    dt = np.complex64 if prec == "c64" else np.complex128
+    for lposs in ((5,), (0, 11), (7, 1), (3, 0, 9), (11, 6, 2)):
+        k = len(lposs)
+        host = [(rng.normal(size=1 << L) + 1j * rng.normal(size=1 << L)).astype(dt) for _ in range(1 << k)]
+        dev = [sim.StateVector(L, h.astype(np.complex128), precision=prec) for h in host]
+        be.remap_local(dev, lposs)
+        ref = [h.copy() for h in host]
+        nb.remap_local(ref, lposs)
+        for d, r in zip(dev, ref):
+            np.testing.assert_array_equal(np.asarray(d.amps).astype(dt), r)
+        for x in range(1 << k):
+            np.testing.assert_array_equal(be.pack_sub(dev[0], lposs, x), nb.pack_sub(ref[0], lposs, x))
+        data = (rng.normal(size=1 << (L - k)) + 1j * rng.normal(size=1 << (L - k))).astype(dt)
+        be.unpack_sub(dev[1], lposs, (1 << k) - 1, data)
+        nb.unpack_sub(ref[1], lposs, (1 << k) - 1, data)
+        np.testing.assert_array_equal(np.asarray(dev[1].amps).astype(dt), ref[1])
+    with pytest.raises(BackendError):
+        be.remap_local(dev[:4], (4, 4))  # repeated local position
+
+
+@pytest.mark.gpu
+def test_nccl_remap_self_peers_and_grouped_sliced_run():
+    """qsb_comm_remap through a 1-rank communicator (every peer = this rank: each region
+    goes out and comes back through NCCL, chunked, all peers in one group), and a sliced
+    RDC16 run with grouped 3-position remaps on one device vs the oracle."""
+    import ctypes
+
+    from paper_2604_11599_b200 import _lib
+
+    ctx = _lib.context()
+    uid = np.zeros(128, dtype=np.uint8)
+    _lib.check(ctx.lib.qsb_comm_unique_id(_lib.ptr(uid)))
+    comm = ctypes.c_void_p()
+    _lib.check(ctx.lib.qsb_comm_init(ctx.handle, _lib.ptr(uid), 0, 1, ctypes.byref(comm)))
+    try:
+        _lib.check(ctx.lib.qsb_comm_set_chunk(comm, 16 << 10))
+        L = 14
+        a0 = np.random.default_rng(4).normal(size=1 << L) + 0j
+        st = sim.StateVector(L, a0)
+        lp = np.array([2, 13, 7], dtype=np.int32)
+        peers = np.zeros(8, dtype=np.int32)
+        _lib.check(ctx.lib.qsb_comm_remap(comm, st._device(), 3, _lib.ptr(lp), _lib.ptr(peers), 0))
+        np.testing.assert_array_equal(st.amps, a0)
+        out = np.zeros(3, dtype=np.int64)
+        _lib.check(ctx.lib.qsb_comm_stats(comm, _lib.ptr(out), None))
+        assert out[0] == 7 * (1 << (L - 3)) * 16 and out[1] == 1
+        bad = np.array([0, 1, 0, 0, 0, 0, 0, 0], dtype=np.int32)  # peer 1 does not exist
+        assert ctx.lib.qsb_comm_remap(comm, st._device(), 3, _lib.ptr(lp), _lib.ptr(bad), 0) != 0
+    finally:
+        ctx.lib.qsb_comm_destroy(comm)
+    _, k = workloads.rdc_circuit(n=16, depth=20, every=10, seed=16)
+    b = ir.bind(k, [])
+    plan = sliced.plan_slices(k, b.values, 3)
+    assert any(len(s[1]) == 3 for s in plan.steps if s[0] == "xchg")
+    rs, ref = P.trajectory(b, P.PortRng.for_shot(1234, 0))
+    store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(1234, 0), 3, plan=plan)
+    assert store.key() == rs.key()
+    np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-10)
