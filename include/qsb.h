@@ -275,6 +275,9 @@ int32_t qsb_slice_scale(qsb_state st, qsb_slicectl c, double re, double im);
 /* this slice's partial p1 of local qubit `qubit` (< 0: its whole norm; select = 0: the
  * slice holds none of the measured amplitudes) into partial slot `index`              */
 int32_t qsb_slice_prob1(qsb_state st, qsb_slicectl c, int32_t qubit, int32_t select, int32_t index);
+/* host read (host_out) and / or write (host_in) of the nslices partial slots, for a
+ * transport that all-gathers them through the host (torch.distributed / gloo)         */
+int32_t qsb_slice_partials(qsb_slicectl c, double* host_out, const double* host_in);
 /* sum the partials in slice order, draw, decide (sim.py:236-248), write the bit       */
 int32_t qsb_slice_decide(qsb_slicectl c, int32_t kind, int32_t bit);
 /* apply the decision: local qubit (flip = reset) or, qubit < 0, a global qubit whose

@@ -130,6 +130,7 @@ _SIGS = {
     "qsb_slice_collapse": (_I32, [_P, _P, _I32, _I32, _I32]),
     "qsb_slice_exchange_local": (_I32, [_P, _P, _I32]),
     "qsb_slice_remap_local": (_I32, [_P, _I32, _P]),
+    "qsb_slice_partials": (_I32, [_P, _P, _P]),
     "qsb_slice_read_sub": (_I32, [_P, _I32, _P, _I32, _P]),
     "qsb_slice_write_sub": (_I32, [_P, _I32, _P, _I32, _P]),
     "qsb_comm_unique_id": (_I32, [_P]),

@@ -151,6 +151,23 @@ int32_t qsb_slice_ctl_read(qsb_slicectl c, uint64_t* bits_out, int32_t* status, 
   return QSB_OK;
 }
 
+// host access to the partial slots (a transport without a device collective: the
+// torch.distributed / gloo path stages them through the host)
+int32_t qsb_slice_partials(qsb_slicectl c, double* host_out, const double* host_in) {
+  if (!c) return fail(QSB_ERR_ARG, "null slicectl");
+  DeviceGuard g(c->ctx->device);
+  const size_t bytes = sizeof(double) * c->nslices;
+  if (host_out) {
+    QSB_CUDA(cudaMemcpyAsync(host_out, c->partials.p, bytes, cudaMemcpyDeviceToHost, c->ctx->stream));
+    QSB_CUDA(cudaStreamSynchronize(c->ctx->stream));
+  }
+  if (host_in) {
+    QSB_CUDA(cudaMemcpyAsync(c->partials.p, host_in, bytes, cudaMemcpyHostToDevice, c->ctx->stream));
+    QSB_CUDA(cudaStreamSynchronize(c->ctx->stream));
+  }
+  return QSB_OK;
+}
+
 int32_t qsb_slice_guard(qsb_slicectl c, const qsb_op* op) {
   if (!c || !op) return fail(QSB_ERR_ARG, "null argument");
   if (op->kind != QSB_OP_IF && op->kind != QSB_OP_ELSE && op->kind != QSB_OP_ENDIF)

@@ -252,7 +252,7 @@ class GpuSliceBackend:
         h = ctypes.c_void_p()
         w = np.ascontiguousarray(rng_words, dtype=np.uint64)
         _l.check(ctx.lib.qsb_slice_ctl_create(ctx.handle, nslices, nbits, 0, 0, _l.ptr(w), ctypes.byref(h)))
-        return _Ctl(ctx, h)
+        return _Ctl(ctx, h, nslices)
 
     def flush(self, st=None) -> None:
         _l = self._lib()
@@ -359,6 +359,19 @@ class GpuSliceBackend:
         lp = np.array(lposs, dtype=np.int32)
         _l.check(st._ctx.lib.qsb_slice_write_sub(st._device(), len(lposs), _l.ptr(lp), int(x), _l.ptr(d)))
 
+    def partials(self, ctl) -> np.ndarray:
+        """Host copy of the partial slots (DistTransport stages the all-gather through
+        the host; `set_partials` writes them back)."""
+        _l = self._lib()
+        out = np.zeros(ctl.nslices, dtype=np.float64)
+        _l.check(ctl.ctx.lib.qsb_slice_partials(ctl.h, _l.ptr(out), None))
+        return out
+
+    def set_partials(self, ctl, values) -> None:
+        _l = self._lib()
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        _l.check(ctl.ctx.lib.qsb_slice_partials(ctl.h, None, _l.ptr(v)))
+
     def read_ctl(self, ctl, nwords: int):
         _l = self._lib()
         bits = np.zeros(max(1, nwords), dtype=np.uint64)
@@ -376,10 +389,10 @@ class GpuSliceBackend:
 class _Ctl:
     """Device SliceCtl handle (destroyed with the object)."""
 
-    def __init__(self, ctx, h):
+    def __init__(self, ctx, h, nslices: int = 1):
         import weakref
 
-        self.ctx, self.h = ctx, h
+        self.ctx, self.h, self.nslices = ctx, h, nslices
         self._fin = weakref.finalize(self, ctx.lib.qsb_slice_ctl_destroy, h)
 
 
@@ -467,7 +480,8 @@ class NcclTransport:
 
 class DistTransport:
     """One slice per rank over torch.distributed (the protocol of NcclTransport with
-    host tensors: gloo in the CPU tests).  The backend provides `partials(ctl)` and
+    host tensors: gloo in the CPU tests, and the device backend staged through the
+    host).  The backend provides `partials(ctl)` (+ `set_partials` for device slots) and
     `pack_sub` / `unpack_sub` of a slice's remap regions."""
 
     def __init__(self):
@@ -486,6 +500,8 @@ class DistTransport:
         self.dist.all_gather(out, torch.tensor([float(part[self.rank])], dtype=torch.float64))
         for s in range(self.nslices):
             part[s] = float(out[s][0])
+        if hasattr(backend, "set_partials"):  # device slots: write the gathered values back
+            backend.set_partials(ctl, part)
 
     def exchange(self, backend, slices, groups, lposs):
         import torch
@@ -497,17 +513,19 @@ class DistTransport:
             st = slices[self.rank]
             me = g.index(self.rank)
             sends, recvs, ops = {}, {}, []
+            dtype = None
             for x, peer in enumerate(g):
                 if x == me:
                     continue
-                data = backend.pack_sub(st, lposs, x)
-                sends[x] = torch.from_numpy(np.ascontiguousarray(data).view(np.float64).copy())
+                data = np.ascontiguousarray(backend.pack_sub(st, lposs, x))
+                dtype = data.dtype  # the slice's precision travels as raw bytes
+                sends[x] = torch.from_numpy(data.view(np.uint8).copy())
                 recvs[x] = torch.empty_like(sends[x])
                 ops += [dist.P2POp(dist.isend, sends[x], peer), dist.P2POp(dist.irecv, recvs[x], peer)]
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
             for x, buf in recvs.items():
-                backend.unpack_sub(st, lposs, x, buf.numpy().view(np.complex128))
+                backend.unpack_sub(st, lposs, x, buf.numpy().view(dtype))
 
 
 # ---------------------------------------------------------------------------

@@ -494,3 +494,60 @@ def test_nccl_remap_self_peers_and_grouped_sliced_run():
     store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(1234, 0), 3, plan=plan)
     assert store.key() == rs.key()
     np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-10)
+
+
+def _gpu_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = []
+        G = world.bit_length() - 1
+        for k in _circuits()[:4]:
+            b = ir.bind(k, [])
+            try:
+                store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(9, 1), G,
+                                                         backend=sliced.GpuSliceBackend(),
+                                                         transport=sliced.DistTransport())
+                res.append((store.key(), st.perm, np.asarray(st.slices[rank].amps).tolist()))
+            except Exception as e:  # DegenerateNorm must agree on every rank
+                res.append((type(e).__name__, None, None))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [2, 4])
+def test_sliced_device_backend_over_ranks(world):
+    """The device slice backend under the multi-rank protocol: one slice per process
+    (all on this GPU; the transport stages remap regions and partial slots through the
+    host with gloo, so no kernel waits on another rank), remaps of 1-2 positions, device
+    decisions from rank-ordered partial sums -- every rank's key and the reassembled
+    state vs the oracle."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=500) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    G = world.bit_length() - 1
+    for ci, k in enumerate(_circuits()[:4]):
+        b = ir.bind(k, [])
+        try:
+            rs, ref = P.trajectory(b, P.PortRng.for_shot(9, 1))
+        except P.DegenerateBranch:
+            assert all(got[r][ci][0] == "DegenerateNorm" for r in range(world))
+            continue
+        assert {got[r][ci][0] for r in range(world)} == {rs.key()}
+        st = sliced.SlicedState.__new__(sliced.SlicedState)
+        st.n, st.G, st.L, st.perm = k.qubit_count, G, k.qubit_count - G, got[0][ci][1]
+        st.backend = NumpyBackend()
+        st.slices = {r: np.array(got[r][ci][2]) for r in range(world)}
+        np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-10)
