@@ -350,9 +350,10 @@ bool edge_x_disabled(const StreamPlan& P) { return P.opt.edge_x == 0; }
 // pass time 607.8 -> 594.5 ms per 2048 shots; no callee-saved spills at phase boundaries)
 // for ~1.7x the NVRTC time; complex64 measured 7 % slower inlined.  $QSB_JIT_INLINE_PHASES
 // = 0 / 1 overrides.
-bool inline_phases(const StreamPlan& P, int c64, int pass_gates) {
+bool inline_phases(const StreamPlan& P, int c64, const PassDesc& pd) {
   if (P.opt.inline_phases >= 0) return P.opt.inline_phases == 1;
-  return !c64 && pass_gates >= P.opt.inline_min_gates;
+  if (P.opt.inline_max_phases > 0 && pd.phase_count > P.opt.inline_max_phases) return false;
+  return !c64 && pd.pgate_count >= P.opt.inline_min_gates;
 }
 
 void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, const PassDesc& pd, int ph_index,
@@ -364,7 +365,7 @@ void emit_phase(std::ostringstream& o, const TapeInfo& t, const StreamPlan& P, c
       << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
          "const int tid, A* __restrict__ dst, const uint64_t* __restrict__ hi_off, MID mid) {\n";
   } else {
-    o << (inline_phases(P, c64, pd.pgate_count) ? "__device__ __forceinline__ void ph" : "__device__ __noinline__ void ph") << ph_index
+    o << (inline_phases(P, c64, pd) ? "__device__ __forceinline__ void ph" : "__device__ __noinline__ void ph") << ph_index
       << "(A* __restrict__ tile, const uint32_t* __restrict__ swz, const qsb::SGate<R>* __restrict__ sg, "
          "const int tid) {\n";
   }

@@ -847,6 +847,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "block_condx") block_condx = v;
   else if (key == "inline_phases") inline_phases = v;
   else if (key == "inline_min_gates") inline_min_gates = v;
+  else if (key == "inline_max_phases") inline_max_phases = v;
   else if (key == "ffma2") ffma2 = v;
   else if (key == "packed_gates") packed_gates = v;
   else if (key == "last_direct") last_direct = v;

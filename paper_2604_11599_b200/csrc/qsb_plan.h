@@ -45,6 +45,7 @@ struct EngineOptions {
   int block_condx = 0;        // a conditional X ends its target's use in a phase
   int inline_phases = -1;     // phases inlined into the pass kernel (-1: complex128 yes, complex64 no)
   int inline_min_gates = 0;   // ... only for passes with at least this many gates
+  int inline_max_phases = 8;  // ... and at most this many phases (0: no limit; VQE24 +2 %, DYN20 / RDC30 neutral)
   int ffma2 = 1;              // complex64 fused blocks as packed fma.rn.f32x2
   int packed_gates = 0;       // complex64 single-gate helpers packed too (bit-identical)
   int last_direct = 1;        // last phase stores to HBM: 0 off, 1 unstaged passes, 2 also staged
@@ -55,7 +56,7 @@ struct EngineOptions {
   int defer_gates = 0;        // gates commuting with a measurement region run after it (measured slower: off)
   uint64_t key() const {
     const int v[] = {pair_aware, phase_search, block_condx, inline_phases, inline_min_gates, ffma2, packed_gates,
-                     last_direct, last_direct_maxlow, minblocks, edge_x, ctas_per_sm, defer_gates};
+                     last_direct, last_direct_maxlow, minblocks, edge_x, ctas_per_sm, defer_gates, inline_max_phases};
     uint64_t h = 1469598103934665603ull;
     for (int x : v) h = (h ^ (uint64_t)(uint32_t)x) * 1099511628211ull;
     return h;
