@@ -551,3 +551,19 @@ def test_sliced_device_backend_over_ranks(world):
         st.backend = NumpyBackend()
         st.slices = {r: np.array(got[r][ci][2]) for r in range(world)}
         np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_sliced_complex64_matches_oracle():
+    """complex64 slices (grouped remaps, device decisions) vs the complex128 oracle
+    within 1e-5 wherever the key agrees; keys agree on these circuits."""
+    for k in _circuits()[:4]:
+        b = ir.bind(k, [])
+        try:
+            rs, ref = P.trajectory(b, P.PortRng.for_shot(9, 2))
+        except P.DegenerateBranch:
+            continue
+        store, st = sliced.run_trajectory_sliced(b, sim.RngStream.for_shot(9, 2), 3,
+                                                 backend=sliced.GpuSliceBackend(precision="c64"))
+        assert store.key() == rs.key()
+        np.testing.assert_allclose(st.gather(), ref.amps, atol=1e-5)
