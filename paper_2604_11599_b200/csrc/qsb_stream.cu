@@ -257,11 +257,29 @@ __global__ void __launch_bounds__(kDT) k_decide(StreamArgs a, RegionDesc rd) {
         if (rd.mloc_bit[j] >= 0) lb |= bit << rd.mloc_bit[j];
         else gv |= (uint64_t)bit << rd.mtile_bit[j];
       }
+      // sum over the tiles in increasing tile order (fixed: run-to-run and batch
+      // invariant); loads issued 8 ahead of the sequential adds
       double s = 0.0;
-      for (int64_t tt = 0; tt < nfree; ++tt) {
-        uint64_t t = pdep64((uint64_t)tt, free_t) | gv;
-        s += part[(int64_t)t * nbl + lb];
+      int64_t tt = 0;
+      if (gm == 0) {  // every measured qubit inside the tile: the tiles are 0 .. nfree-1
+        const double* pp = part + lb;
+        for (; tt + 8 <= nfree; tt += 8) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = pp[(tt + u) * nbl];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += x[u];
+        }
+      } else {
+        for (; tt + 8 <= nfree; tt += 8) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = part[(int64_t)(pdep64((uint64_t)(tt + u), free_t) | gv) * nbl + lb];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += x[u];
+        }
       }
+      for (; tt < nfree; ++tt) s += part[(int64_t)(pdep64((uint64_t)tt, free_t) | gv) * nbl + lb];
       marg[b] = s;
     }
   }
@@ -399,27 +417,59 @@ __global__ void __launch_bounds__(kDT) k_decide(StreamArgs a, RegionDesc rd) {
 // becomes a representative while its state lived elsewhere copies the (pre-collapse)
 // buffer of its old representative, then applies its own collapse in the next pass.
 // The arithmetic per trajectory is unchanged, so results are bit-identical.
-__global__ void k_dedup_regroup(StreamArgs a, int32_t* new_rep, int32_t* copy_src) {
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= a.slots) return;
-  const TrajCtl c = a.ctl[s];
+// One thread per slot scans the lower slots for the first one with its history; the
+// candidates' keys (alive, draws, hash) are staged through shared memory a tile of
+// kRegroupTile slots at a time (one coalesced load per tile for the whole block instead
+// of three dependent global loads per candidate per thread), and the block stops as soon
+// as every thread has its representative.  Same result as the plain scan: the lowest
+// alive slot with the same exact history.
+constexpr int kRegroupTile = 256;
+
+__global__ void __launch_bounds__(kRegroupTile) k_dedup_regroup(StreamArgs a, int32_t* new_rep, int32_t* copy_src) {
+  __shared__ uint64_t kh[kRegroupTile];
+  __shared__ int32_t kd[kRegroupTile];
+  const int64_t s = blockIdx.x * (int64_t)kRegroupTile + threadIdx.x;
+  const bool valid = s < a.slots;
+  uint64_t hist = 0;
+  int32_t draws = 0, status = 1, rep = 0;
+  if (valid) {
+    const TrajCtl& c = a.ctl[s];
+    hist = c.hist;
+    draws = c.draws;
+    status = c.status;
+    rep = c.rep;
+  }
   int32_t r = (int32_t)s;
-  if (c.status == 0) {
-    for (int64_t t = 0; t < s; ++t) {
-      const TrajCtl& o = a.ctl[t];
-      if (o.status == 0 && o.hist == c.hist && o.draws == c.draws) {
+  bool done = !valid || status != 0;
+  const int64_t smax = blockIdx.x * (int64_t)kRegroupTile;  // candidates below the block (own tile: below)
+  for (int64_t t0 = 0; t0 <= smax; t0 += kRegroupTile) {
+    if (__syncthreads_and(done)) break;
+    const int64_t t = t0 + threadIdx.x;
+    const bool alive = t < a.slots && a.ctl[t].status == 0;
+    kh[threadIdx.x] = alive ? a.ctl[t].hist : 0;
+    kd[threadIdx.x] = alive ? a.ctl[t].draws : -1;  // draws >= 0: a dead slot never matches
+    __syncthreads();
+    if (!done) {
+      const int64_t rem = s - t0;  // candidates t < s only
+      const int lim = rem < kRegroupTile ? (int)rem : kRegroupTile;
+      for (int j = 0; j < lim; ++j) {
+        if (kd[j] != draws || kh[j] != hist) continue;
         // the 64-bit hash is only a filter: merge on the exact outcome history
+        const int64_t u = t0 + j;
         bool same = true;
-        for (int w = 0; w < a.hwords && same; ++w) same = a.hbits[t * a.hwords + w] == a.hbits[s * a.hwords + w];
+        for (int w = 0; w < a.hwords && same; ++w) same = a.hbits[u * a.hwords + w] == a.hbits[s * a.hwords + w];
         if (same) {
-          r = (int32_t)t;
+          r = (int32_t)u;
+          done = true;
           break;
         }
       }
     }
+    __syncthreads();
   }
+  if (!valid) return;
   new_rep[s] = r;
-  copy_src[s] = (r == s && c.rep != s && c.status == 0) ? c.rep : -1;
+  copy_src[s] = (r == s && rep != s && status == 0) ? rep : -1;
 }
 
 __global__ void k_dedup_copy(StreamArgs a, const int32_t* copy_src, int64_t amp_bytes) {
@@ -506,7 +556,8 @@ void launch_dedup(const StreamArgs& a, int32_t* new_rep, int32_t* copy_src, int3
                   int c64, bool regroup, cudaStream_t s) {
   const unsigned g = (unsigned)((a.slots + 127) / 128);
   if (regroup) {
-    k_dedup_regroup<<<g, 128, 0, s>>>(a, new_rep, copy_src);
+    k_dedup_regroup<<<(unsigned)((a.slots + kRegroupTile - 1) / kRegroupTile), kRegroupTile, 0, s>>>(a, new_rep,
+                                                                                                   copy_src);
     const int64_t amp = c64 ? 8 : 16;
     const int64_t words = (amp << a.n) / 16;
     unsigned chunks = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 2048), 64);
