@@ -258,7 +258,7 @@ int alloc_stream_scratch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, in
   QSB_CUDA(ctx->guards.ensure(sizeof(uint32_t) * t.gwords * slots));
   int64_t pstride = ((int64_t)1 << P.ntiles_log2) * P.max_local_bins;
   QSB_CUDA(ctx->partial.ensure(sizeof(double) * pstride * slots));
-  QSB_CUDA(ctx->dedup.ensure(sizeof(int32_t) * (3 * slots + 4)));
+  QSB_CUDA(ctx->dedup.ensure(sizeof(int32_t) * (5 * slots + 8)));
   return QSB_OK;
 }
 
@@ -300,6 +300,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   int32_t* d_copy_src = d_new_rep + r.slots;
   int32_t* d_active = d_copy_src + r.slots;
   int32_t* d_nactive = d_active + r.slots;
+  int32_t* d_split = d_nactive + 4;  // [branches | others | 2 counts] (launch_dedup)
   double* d_phys = reinterpret_cast<double*>(ctx->counters.as<char>() + 16);  // [bytes, flops] physical
   if (dedup) {  // outcome-history rows: one bit per draw (measure / reset ops bound the draws)
     int ndraw_ops = 0;
@@ -315,7 +316,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   if (dedup) {
     a.active = d_active;
     a.nactive = d_nactive;
-    launch_dedup(a, d_new_rep, d_copy_src, d_active, d_nactive, r.c64, false, ctx->stream);
+    launch_dedup(a, d_new_rep, d_copy_src, d_active, d_nactive, r.c64, false, nullptr, ctx->stream);
     r.launches += 2;
   }
   r.physical_counted = dedup;
@@ -333,15 +334,35 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   uint64_t acc = 0;
   int consumed = 0;
   const double state_bytes = (double)amp_bytes(r.c64) * (double)((int64_t)1 << t.n) * (double)r.slots;
-  for (const Step& s : P.steps) {
+  bool split_next = false;  // the next pass starts the branches of the last regroup
+  for (size_t si = 0; si < P.steps.size(); ++si) {
+    const Step& s = P.steps[si];
     if (s.type == 0) {
       PassDesc pd = P.passes[s.index];
       if (r.in_place) pd.init_zero = 0;
       cudaEventRecord(ctx->pass_events[2 * s.index], ctx->stream);
-      if (s.index < (int)r.pd->jit.size() && r.pd->jit[s.index].kern)
-        QSB_CUDA(jit_launch(r.pd->jit[s.index], a, pd, ctx->stream));
-      else
-        QSB_CUDA(launch_pass(a, pd, ctx->stream));
+      auto launch = [&](const StreamArgs& x) -> cudaError_t {
+        if (s.index < (int)r.pd->jit.size() && r.pd->jit[s.index].kern) return jit_launch(r.pd->jit[s.index], x, pd, ctx->stream);
+        return launch_pass(x, pd, ctx->stream);
+      };
+      if (split_next) {
+        // branches first (gather from the old representative's buffer, write their own),
+        // then the other representatives in place -- every read of a buffer precedes its
+        // overwrite by the stream order of the two launches
+        StreamArgs b = a;
+        b.active = d_split;
+        b.nactive = d_split + 2 * r.slots;
+        b.read_src = d_copy_src;
+        QSB_CUDA(launch(b));
+        b.active = d_split + r.slots;
+        b.nactive = d_split + 2 * r.slots + 1;
+        b.read_src = nullptr;
+        QSB_CUDA(launch(b));
+        r.launches++;
+        split_next = false;
+      } else {
+        QSB_CUDA(launch(a));
+      }
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
       r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
       ctx->run_flops += r.pd->pflops[s.index] * (double)r.slots;
@@ -360,8 +381,13 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
       r.decides++;
       r.launches++;
       if (dedup) {
-        launch_dedup(a, d_new_rep, d_copy_src, d_active, d_nactive, r.c64, true, ctx->stream);
-        r.launches += 4;
+        // a pass next: it reads the old buffers itself (no state copies); else copy now
+        // (register-phase passes only: the shared-memory fallback kernel walks every slot)
+        split_next = ctx->opt_defer_copy && si + 1 < P.steps.size() && P.steps[si + 1].type == 0 && !r.in_place &&
+                     a.phases && P.passes[P.steps[si + 1].index].rb > 0;
+        launch_dedup(a, d_new_rep, d_copy_src, d_active, d_nactive, r.c64, true, split_next ? d_split : nullptr,
+                     ctx->stream);
+        r.launches += split_next ? 2 : 3;  // regroup (+ copy) + commit
       }
       acc = 0;
       consumed = 0;
@@ -510,7 +536,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
-  else if (k == "jit_async") ctx->opt_jit_async = value;  // NVRTC in the background, generic kernel meanwhile
+  else if (k == "jit_async") ctx->opt_jit_async = value;
+  else if (k == "defer_copy") ctx->opt_defer_copy = value;  // dedup: branches read the old buffer in their first pass  // NVRTC in the background, generic kernel meanwhile
   else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles
   else if (k == "expval_jit") ctx->opt_ev_jit = value;          // NVRTC-specialised Pauli reducer
   else if (k == "expval_jit_terms") ctx->opt_ev_jit_terms = value;  // its terms per launch (<= 32)

@@ -220,6 +220,8 @@ struct StreamArgs {
   // active[0 .. *nactive) (null: every slot)
   const int32_t* active;
   const int32_t* nactive;
+  // per slot: the slot whose buffer its gather reads (< 0 or null: its own)
+  const int32_t* read_src;
   // ... whose keys are verified on the exact outcome history: bit d of slot s's row is
   // the outcome of its d-th draw (null: no dedup)
   uint64_t* hbits;

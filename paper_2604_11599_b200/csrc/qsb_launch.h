@@ -127,9 +127,12 @@ void launch_mats_prep(const MatSrc* src, int nmat, const double* params, int npa
 void launch_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards, int gwords, int64_t slots,
                      uint64_t seed, int64_t shot_begin, const uint64_t* rng_init, int dedup, cudaStream_t s);
 // history dedup bookkeeping: regroup + copy (after a decide) or initial grouping, then
-// the representative list the passes iterate
+// the representative list the passes iterate.  split != null (regroup before a pass):
+// no copies -- the new branches and the other representatives are listed apart
+// (k_dedup_commit) and the next pass runs as two launches, the branches first, reading
+// their old representatives' buffers (StreamArgs::read_src = copy_src)
 void launch_dedup(const StreamArgs& a, int32_t* new_rep, int32_t* copy_src, int32_t* active, int32_t* nactive,
-                  int c64, bool regroup, cudaStream_t s);
+                  int c64, bool regroup, int32_t* split, cudaStream_t s);
 // physical pass work under dedup: phys[0] += bytes_per_state * nactive, phys[1] += flops * nactive
 void launch_accum_physical(const int32_t* nactive, double flops_per_state, double bytes_per_state, double* phys,
                            cudaStream_t s);

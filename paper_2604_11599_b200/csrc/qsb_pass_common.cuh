@@ -57,6 +57,7 @@ template <typename R> struct PassCtx {
 // per work-item (slot, tile) view of the trajectory control block
 struct PassItem {
   int64_t slot;
+  int64_t src;  // slot whose buffer the gather reads (history dedup: a branch's first pass)
   uint64_t base_phys, base_log, Kp, Vp;
   uint32_t fl;
   bool alive, pending;
@@ -107,7 +108,7 @@ __device__ __forceinline__ uint32_t tab32(const uint32_t* t, uint64_t x, int nbi
 // the per-state part of an item's context (one TrajCtl read)
 struct SlotCtx {
   int64_t idx;  // active-list index (w >> ntl)
-  int64_t slot;
+  int64_t slot, src;
   uint64_t F, Kp, Vp;
   double sre, sim;
   bool alive, pending;
@@ -117,6 +118,10 @@ __device__ __forceinline__ SlotCtx slot_ctx(const StreamArgs& a, const PassDesc&
   SlotCtx s;
   s.idx = idx;
   s.slot = a.active ? a.active[idx] : idx;  // representative slots only (history dedup)
+  // a branch that just split off its representative reads the representative's
+  // (pre-collapse) buffer in its first pass instead of a copy of it
+  const int32_t rs = a.read_src ? a.read_src[s.slot] : -1;
+  s.src = rs >= 0 ? rs : s.slot;
   const TrajCtl* c = a.ctl + s.slot;
   s.alive = c->status == 0;
   s.F = c->frame & ~pd.clear_before;
@@ -132,6 +137,7 @@ __device__ __forceinline__ PassItem item_of(const SlotCtx& s, const PassDesc& pd
                                             const ItemTables& tb) {
   PassItem it;
   it.slot = s.slot;
+  it.src = s.src;
   it.alive = s.alive;
   it.pending = s.pending;
   it.Kp = s.Kp;
@@ -276,7 +282,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
 
   auto prefetch = [&](const PassItem& it, A* dst) {
     if (!it.alive) return;
-    const A* st = reinterpret_cast<const A*>(a.state) + (it.slot << a.n);
+    const A* st = reinterpret_cast<const A*>(a.state) + (it.src << a.n);
     const uint64_t pb = it.base_phys | Pt;
     const uint32_t fb = flip_base(it.fl);
 #pragma unroll 4

@@ -488,12 +488,23 @@ __global__ void k_dedup_init_rep(StreamArgs a, int32_t* new_rep) {
   if (s < a.slots) new_rep[s] = a.ctl[s].rep;
 }
 
-__global__ void k_dedup_commit(StreamArgs a, const int32_t* new_rep, int32_t* active, int32_t* nactive) {
+// split != null (deferred copies): the representatives are also listed apart -- split[0 ..)
+// the new branches (copy_src >= 0: their first pass reads the old representative's
+// buffer), split[slots ..) the rest, counts at split[2 slots], split[2 slots + 1]
+__global__ void k_dedup_commit(StreamArgs a, const int32_t* new_rep, int32_t* active, int32_t* nactive,
+                               const int32_t* copy_src, int32_t* split) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= a.slots) return;
   const int32_t r = new_rep[s];
   a.ctl[s].rep = r;
-  if (r == s && a.ctl[s].status == 0) active[atomicAdd(nactive, 1)] = (int32_t)s;  // order is irrelevant
+  if (r == s && a.ctl[s].status == 0) {
+    active[atomicAdd(nactive, 1)] = (int32_t)s;  // order is irrelevant
+    if (split) {
+      const bool branch = copy_src[s] >= 0;
+      int32_t* cnt = split + 2 * a.slots + (branch ? 0 : 1);
+      split[(branch ? 0 : a.slots) + atomicAdd(cnt, 1)] = (int32_t)s;
+    }
+  }
 }
 
 __global__ void k_count(StreamArgs a, const int32_t* guard_gates, int nguards, int64_t unguarded,
@@ -553,20 +564,24 @@ void launch_accum_physical(const int32_t* nactive, double flops_per_state, doubl
 }
 
 void launch_dedup(const StreamArgs& a, int32_t* new_rep, int32_t* copy_src, int32_t* active, int32_t* nactive,
-                  int c64, bool regroup, cudaStream_t s) {
+                  int c64, bool regroup, int32_t* split, cudaStream_t s) {
   const unsigned g = (unsigned)((a.slots + 127) / 128);
   if (regroup) {
     k_dedup_regroup<<<(unsigned)((a.slots + kRegroupTile - 1) / kRegroupTile), kRegroupTile, 0, s>>>(a, new_rep,
                                                                                                    copy_src);
-    const int64_t amp = c64 ? 8 : 16;
-    const int64_t words = (amp << a.n) / 16;
-    unsigned chunks = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 2048), 64);
-    k_dedup_copy<<<dim3(chunks, (unsigned)a.slots), 256, 0, s>>>(a, copy_src, amp);
+    if (!split) {  // copies now (no pass follows that could read the old buffers)
+      const int64_t amp = c64 ? 8 : 16;
+      const int64_t words = (amp << a.n) / 16;
+      unsigned chunks = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 2048), 64);
+      k_dedup_copy<<<dim3(chunks, (unsigned)a.slots), 256, 0, s>>>(a, copy_src, amp);
+    }
   } else {  // initial grouping from ctl.rep
     k_dedup_init_rep<<<g, 128, 0, s>>>(a, new_rep);
+    split = nullptr;
   }
   cudaMemsetAsync(nactive, 0, sizeof(int32_t), s);
-  k_dedup_commit<<<g, 128, 0, s>>>(a, new_rep, active, nactive);
+  if (split) cudaMemsetAsync(split + 2 * a.slots, 0, 2 * sizeof(int32_t), s);
+  k_dedup_commit<<<g, 128, 0, s>>>(a, new_rep, active, nactive, copy_src, split);
 }
 
 static size_t pass_smem(int c64, const PassDesc& pd) {
