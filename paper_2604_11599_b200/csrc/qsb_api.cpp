@@ -413,6 +413,11 @@ double pass_ms_sum(qsb_ctx ctx, size_t npasses) {
 
 int64_t pick_batch(qsb_ctx ctx, const TapeInfo& t, const StreamPlan& P, int c64, int64_t count) {
   if (ctx->opt_batch > 0) return std::min<int64_t>(ctx->opt_batch, count);
+  // the whole job already fits the buffers this context holds: no driver query
+  // (cudaMemGetInfo takes 0.1 to tens of ms -- GPU idle time inside a timed call)
+  if ((double)ctx->state.bytes >= (double)amp_bytes(c64) * std::ldexp(1.0, t.n) * (double)count &&
+      (double)ctx->partial.bytes >= 8.0 * std::ldexp(1.0, P.ntiles_log2) * P.max_local_bins * (double)count)
+    return count;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   // already-held scratch counts as available
