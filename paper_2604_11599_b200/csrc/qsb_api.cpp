@@ -340,6 +340,15 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
     if (s.type == 0) {
       PassDesc pd = P.passes[s.index];
       if (r.in_place) pd.init_zero = 0;
+      // register-phase init pass: zero the states, then compute only the tile holding
+      // index 0 of each (every other tile of |0...0> stays zero under in-tile gates)
+      const bool tile0 = pd.init_zero && a.phases && pd.rb > 0;
+      const double pass_frac = tile0 ? std::ldexp(1.0, -P.ntiles_log2) : 1.0;  // executed share of the flops
+      if (tile0) {
+        launch_zero_slots(a, r.c64, pd.epi ? 1 : 0, ctx->stream);
+        r.launches++;
+        pd.init_zero = 2;
+      }
       cudaEventRecord(ctx->pass_events[2 * s.index], ctx->stream);
       auto launch = [&](const StreamArgs& x) -> cudaError_t {
         if (s.index < (int)r.pd->jit.size() && r.pd->jit[s.index].kern) return jit_launch(r.pd->jit[s.index], x, pd, ctx->stream);
@@ -365,9 +374,9 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
       }
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
       r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
-      ctx->run_flops += r.pd->pflops[s.index] * (double)r.slots;
+      ctx->run_flops += r.pd->pflops[s.index] * pass_frac * (double)r.slots;
       if (dedup) {  // the kernels touched only the representatives
-        launch_accum_physical(d_nactive, r.pd->pflops[s.index],
+        launch_accum_physical(d_nactive, r.pd->pflops[s.index] * pass_frac,
                               (pd.init_zero ? 1.0 : 2.0) * state_bytes / (double)r.slots, d_phys, ctx->stream);
         r.launches++;
       }

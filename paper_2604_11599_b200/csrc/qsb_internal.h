@@ -134,7 +134,7 @@ struct PassDesc {
   int32_t sq[kMaxTile]; // local bit j -> qubit
   int32_t gate_begin, gate_count;
   int32_t prologue;     // apply the pending collapse of the previous decide
-  int32_t init_zero;    // input is |0...0> (first pass): no read
+  int32_t init_zero;    // input is |0...0> (first pass): no read; 2: states pre-zeroed, tile 0 only
   int32_t epi;          // compute the marginal of mmask in the epilogue
   int32_t m_local;      // |M ∩ S|
   int32_t mloc[kMaxMeasureRegion];   // local positions of M∩S, in M order

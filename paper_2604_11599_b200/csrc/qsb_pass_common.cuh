@@ -273,7 +273,13 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   const int hstep = T >> pd.lowq;
   __syncthreads();
   const int ntl = a.n - k;
-  const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << ntl;
+  // init_zero == 2: the input is |0...0> and the caller zeroed the states, so only the
+  // tile holding index 0 can become nonzero (gates stay inside a tile): one item per slot
+  const bool tile0 = pd.init_zero == 2;
+  const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << (tile0 ? 0 : ntl);
+  auto item_at = [&](int64_t w) -> PassItem {
+    return tile0 ? item_of(slot_ctx(a, pd, w), pd, 0, ntl, a.n, itb) : pass_item(a, pd, w, ntl, itb);
+  };
 
   // swizzled-slot base of this thread for an item with frame flip fl
   auto flip_base = [&](uint32_t fl) -> uint32_t {
@@ -431,7 +437,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   int64_t w = blockIdx.x;
   PassItem cur;
   cur.alive = false;
-  if (w < W) cur = pass_item(a, pd, w, ntl, itb);
+  if (w < W) cur = item_at(w);
   if (w < W) prefetch(cur, bufs);
   cp_async_commit();
   int b = 0;
@@ -439,7 +445,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
     const int64_t wn = w + gridDim.x;
     PassItem nxt;
     nxt.alive = false;
-    if (wn < W) nxt = pass_item(a, pd, wn, ntl, itb);
+    if (wn < W) nxt = item_at(wn);
     if (NB == 2) {
       if (wn < W) prefetch(nxt, bufs + (b ^ 1) * TL);
       cp_async_commit();

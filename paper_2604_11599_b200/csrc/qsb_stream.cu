@@ -558,6 +558,31 @@ __global__ void k_accum_physical(const int32_t* nactive, double flops, double by
   phys[1] += flops * (double)*nactive;
 }
 
+// zero the state (and the epilogue partials) of the active slots: the init pass then
+// computes only the tile holding index 0 of each (PassDesc::init_zero == 2)
+__global__ void k_zero_slots(StreamArgs a, int64_t amp_words, int zero_partials) {
+  const int64_t n_act = a.active ? *a.nactive : a.slots;
+  for (int64_t si = blockIdx.y; si < n_act; si += gridDim.y) {
+    const int64_t slot = a.active ? a.active[si] : si;
+    int4* st = reinterpret_cast<int4*>(a.state) + slot * amp_words;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < amp_words; i += (int64_t)gridDim.x * blockDim.x)
+      st[i] = make_int4(0, 0, 0, 0);
+    if (zero_partials) {
+      double* pp = a.partial + slot * a.partial_stride;
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.partial_stride;
+           i += (int64_t)gridDim.x * blockDim.x)
+        pp[i] = 0.0;
+    }
+  }
+}
+
+void launch_zero_slots(const StreamArgs& a, int c64, int zero_partials, cudaStream_t s) {
+  const int64_t words = ((int64_t)(c64 ? 8 : 16) << a.n) / 16;
+  const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 1024), 64);
+  const unsigned gy = (unsigned)std::min<int64_t>(a.slots, 65535);
+  k_zero_slots<<<dim3(gx, gy), 256, 0, s>>>(a, words, zero_partials);
+}
+
 void launch_accum_physical(const int32_t* nactive, double flops_per_state, double bytes_per_state, double* phys,
                            cudaStream_t s) {
   k_accum_physical<<<1, 1, 0, s>>>(nactive, flops_per_state, bytes_per_state, phys);
