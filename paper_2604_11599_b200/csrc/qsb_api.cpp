@@ -772,31 +772,104 @@ int expval_terms_tiled(qsb_ctx ctx, int c64, const void* amps, int n, int64_t sl
                        const uint64_t* zm, const int32_t* ny, int nterm, double* out_host) {
   const int k = std::min(12, n), lowq = std::min((int)(ctx->opt_ev_lowq > 0 ? ctx->opt_ev_lowq : 2), k);
   const uint64_t lowmask = (1ull << lowq) - 1;
-  std::vector<int> order(nterm);
-  for (int t = 0; t < nterm; ++t) order[t] = t;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    return __builtin_popcountll(xm[a]) > __builtin_popcountll(xm[b]);
-  });
   struct Grp { uint64_t S; std::vector<int> terms; };
   std::vector<Grp> groups;
-  std::vector<int> diag;
-  for (int t : order) {
-    if (xm[t] == 0) {
-      diag.push_back(t);
-      continue;
-    }
-    bool placed = false;
-    for (Grp& g : groups)
-      if (__builtin_popcountll(g.S | xm[t]) <= k) {
-        g.S |= xm[t];
-        g.terms.push_back(t);
-        placed = true;
-        break;
-      }
-    if (!placed) groups.push_back({lowmask | xm[t], {t}});
+  // Tile sets (each launch reads every state once, whatever its term count, so the
+  // number of launches is the cost): greedy maximum coverage -- grow a k-qubit set from
+  // the low run one qubit at a time, each time the qubit that completes the most
+  // uncovered X-supports (ties: the most support bits inside), until every term is
+  // covered; then every term goes to one set that contains its X-support, single-choice
+  // terms first, the others where the current launch of cap terms has room.  VQE24's 200
+  // terms: 12 -> 9 launches per state (first-fit by X weight before).
+  // (the NVRTC launch size, also when the generic kernel runs: the grouping -- and so the
+  // per-term arithmetic -- must not depend on which kernel evaluates it)
+  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(32, ctx->opt_ev_jit_terms));
+  std::vector<int> left, diag, wide_sup;
+  for (int t = 0; t < nterm; ++t) {
+    if (xm[t] == 0) diag.push_back(t);
+    else if (__builtin_popcountll(xm[t] | lowmask) > k) wide_sup.push_back(t);  // fits no tile
+    else left.push_back(t);
   }
-  if (groups.empty()) groups.push_back({lowmask, {}});
-  for (int t : diag) groups[0].terms.push_back(t);
+  while (!left.empty()) {
+    uint64_t S = lowmask;
+    while (__builtin_popcountll(S) < k) {
+      int best_q = -1;
+      long best_cov = -1, best_part = -1;
+      for (int q = 0; q < n; ++q) {
+        if (S >> q & 1) continue;
+        const uint64_t T = S | (1ull << q);
+        long cov = 0, part = 0;
+        for (int t : left) {
+          if ((xm[t] & ~T) == 0) ++cov;
+          else part += __builtin_popcountll(xm[t] & T);
+        }
+        if (cov > best_cov || (cov == best_cov && part > best_part)) {
+          best_q = q;
+          best_cov = cov;
+          best_part = part;
+        }
+      }
+      if (best_q < 0) break;
+      S |= 1ull << best_q;
+    }
+    std::vector<int> rest;
+    bool any = false;
+    for (int t : left) {
+      if ((xm[t] & ~S) == 0) any = true;
+      else rest.push_back(t);
+    }
+    if (!any) {  // cannot happen (the first support fits a tile), but never loop forever
+      S = lowmask | xm[left[0]];
+      for (int q = 0; q < n && __builtin_popcountll(S) < k; ++q) S |= 1ull << q;
+      rest.clear();
+      for (int t : left)
+        if ((xm[t] & ~S) != 0) rest.push_back(t);
+    }
+    groups.push_back({S, {}});
+    left.swap(rest);
+  }
+  if (groups.empty()) {
+    uint64_t S = lowmask;
+    for (int q = 0; q < n && __builtin_popcountll(S) < k; ++q) S |= 1ull << q;
+    groups.push_back({S, {}});
+  }
+  {
+    std::vector<int> cnt(groups.size(), 0), flex;
+    std::vector<std::vector<int>> feas(nterm);
+    for (int t = 0; t < nterm; ++t) {
+      if (__builtin_popcountll(xm[t] | lowmask) > k) continue;
+      for (size_t i = 0; i < groups.size(); ++i)
+        if ((xm[t] & ~groups[i].S) == 0) feas[t].push_back((int)i);
+      if (feas[t].size() == 1) {
+        groups[feas[t][0]].terms.push_back(t);
+        cnt[feas[t][0]]++;
+      } else if (!feas[t].empty()) {
+        flex.push_back(t);
+      }
+    }
+    std::stable_sort(flex.begin(), flex.end(), [&](int a, int b) { return feas[a].size() < feas[b].size(); });
+    for (int t : flex) {
+      int best = feas[t][0];
+      auto score = [&](int i) {  // prefer a launch with room (most terms already in it), not a fresh one
+        const int r = cnt[i] % cap;
+        return (cnt[i] > 0 && r == 0) ? -1 : r;
+      };
+      for (int i : feas[t])
+        if (score(i) > score(best)) best = i;
+      groups[best].terms.push_back(t);
+      cnt[best]++;
+    }
+    // keep each group's terms in the historical order (by X weight, descending)
+    for (Grp& g : groups)
+      std::stable_sort(g.terms.begin(), g.terms.end(), [&](int a, int b) {
+        return __builtin_popcountll(xm[a]) > __builtin_popcountll(xm[b]);
+      });
+    std::vector<Grp> kept;
+    for (Grp& g : groups)
+      if (!g.terms.empty()) kept.push_back(std::move(g));
+    groups.swap(kept);
+  }
+  for (int t : wide_sup) groups.push_back({lowmask | xm[t], {t}});  // > k support bits: pair-loop path
   std::vector<ExpvalTerm> dev_terms, by_out(nterm);
   std::vector<ExpvalGroup> dev_groups;  // pair-loop launches (path 1)
   std::vector<ExpvalGroup> acc_groups;  // accumulating launches (path 0, k = 12)
