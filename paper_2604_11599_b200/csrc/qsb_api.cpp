@@ -335,19 +335,43 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   int consumed = 0;
   const double state_bytes = (double)amp_bytes(r.c64) * (double)((int64_t)1 << t.n) * (double)r.slots;
   bool split_next = false;  // the next pass starts the branches of the last regroup
+  // qubits still |0> since the |0...0> start (none for an in-place run)
+  uint64_t untouched = r.in_place ? 0 : ((t.n >= 64) ? ~0ull : ((1ull << t.n) - 1));
+  bool zeroed = false;  // states zeroed before the first pass (the skipped items hold zeros)
   for (size_t si = 0; si < P.steps.size(); ++si) {
     const Step& s = P.steps[si];
     if (s.type == 0) {
       PassDesc pd = P.passes[s.index];
       if (r.in_place) pd.init_zero = 0;
-      // register-phase init pass: zero the states, then compute only the tile holding
-      // index 0 of each (every other tile of |0...0> stays zero under in-tile gates)
-      const bool tile0 = pd.init_zero && a.phases && pd.rb > 0;
-      const double pass_frac = tile0 ? std::ldexp(1.0, -P.ntiles_log2) : 1.0;  // executed share of the flops
-      if (tile0) {
-        launch_zero_slots(a, r.c64, pd.epi ? 1 : 0, ctx->stream);
-        r.launches++;
-        pd.init_zero = 2;
+      // From the |0...0> start until the first decide, qubits no non-diagonal gate has
+      // touched are still |0>: the states are zeroed once before the first pass, and every
+      // register-phase pass then runs only the items whose tile id has none of those
+      // qubits set (the first pass: the tile holding index 0; gates act inside a tile, so
+      // the other items stay exactly zero).  Not for passes with an epilogue (their
+      // marginal partials cover every tile).
+      pd.zero_tid = 0;
+      const bool skippable = a.phases && pd.rb > 0 && !pd.epi && untouched;
+      if (pd.init_zero) {
+        if (skippable) {
+          launch_zero_slots(a, r.c64, 0, ctx->stream);
+          r.launches++;
+          zeroed = true;
+        }
+      }
+      if (skippable && zeroed) {
+        int j = 0;
+        for (int q = 0; q < t.n; ++q) {
+          if (pd.smask >> q & 1) continue;
+          if (untouched >> q & 1) pd.zero_tid |= 1ull << j;
+          ++j;
+        }
+      }
+      const double pass_frac = std::ldexp(1.0, -__builtin_popcountll(pd.zero_tid));  // executed share of the flops
+      for (int g = pd.gate_begin; g < pd.gate_begin + pd.gate_count; ++g) {  // qubits this pass can move
+        const PassGate& q = P.gates[g];
+        if (q.gclass == GC_DIAG || q.gclass == GC_DIAG_GLOBAL) continue;
+        if (q.lt >= 0) untouched &= ~(1ull << pd.sq[q.lt]);
+        if (q.gclass == GC_SWAP && q.lt2 >= 0) untouched &= ~(1ull << pd.sq[q.lt2]);
       }
       cudaEventRecord(ctx->pass_events[2 * s.index], ctx->stream);
       auto launch = [&](const StreamArgs& x) -> cudaError_t {
@@ -400,6 +424,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
       }
       acc = 0;
       consumed = 0;
+      if (rd.op_end > rd.op_begin) untouched = 0;  // after a measurement: no known-zero qubits
     }
   }
   r.final_clear = acc;

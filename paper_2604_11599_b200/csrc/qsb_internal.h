@@ -134,12 +134,16 @@ struct PassDesc {
   int32_t sq[kMaxTile]; // local bit j -> qubit
   int32_t gate_begin, gate_count;
   int32_t prologue;     // apply the pending collapse of the previous decide
-  int32_t init_zero;    // input is |0...0> (first pass): no read; 2: states pre-zeroed, tile 0 only
+  int32_t init_zero;    // input is |0...0> (first pass): no read
   int32_t epi;          // compute the marginal of mmask in the epilogue
   int32_t m_local;      // |M ∩ S|
   int32_t mloc[kMaxMeasureRegion];   // local positions of M∩S, in M order
   int32_t region;       // decide region fed by the epilogue
   int32_t rb;           // register bits of the phases (0: no phases, shared-memory kernel)
+  // tile-id bits of qubits still in |0> (no non-diagonal gate on them since the |0...0>
+  // start; set by the host per run): every item with one of them set is zero before and
+  // after the pass and its buffer already holds zeros -- only the others run
+  uint64_t zero_tid;
 };
 
 struct RegionDesc {

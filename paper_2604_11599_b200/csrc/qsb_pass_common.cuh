@@ -273,12 +273,17 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   const int hstep = T >> pd.lowq;
   __syncthreads();
   const int ntl = a.n - k;
-  // init_zero == 2: the input is |0...0> and the caller zeroed the states, so only the
-  // tile holding index 0 can become nonzero (gates stay inside a tile): one item per slot
-  const bool tile0 = pd.init_zero == 2;
-  const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << (tile0 ? 0 : ntl);
+  // pd.zero_tid: the items whose tile id has one of these bits set are known zero (qubits
+  // still in |0>, buffers pre-zeroed): enumerate only the others -- the tile id is the
+  // item's free bits deposited around the zero ones (the init pass: tile 0 only)
+  const uint64_t tid_all = (ntl >= 64) ? ~0ull : ((1ull << ntl) - 1);
+  const uint64_t tid_free = tid_all & ~pd.zero_tid;
+  const int ntl_run = __popcll(tid_free);
+  const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << ntl_run;
   auto item_at = [&](int64_t w) -> PassItem {
-    return tile0 ? item_of(slot_ctx(a, pd, w), pd, 0, ntl, a.n, itb) : pass_item(a, pd, w, ntl, itb);
+    if (!pd.zero_tid) return pass_item(a, pd, w, ntl, itb);
+    const uint64_t tile = pdep64((uint64_t)w & ((1ull << ntl_run) - 1), tid_free);
+    return item_of(slot_ctx(a, pd, w >> ntl_run), pd, tile, ntl, a.n, itb);
   };
 
   // swizzled-slot base of this thread for an item with frame flip fl
