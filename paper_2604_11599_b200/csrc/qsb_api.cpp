@@ -338,6 +338,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   // qubits still |0> since the |0...0> start (none for an in-place run)
   uint64_t untouched = r.in_place ? 0 : ((t.n >= 64) ? ~0ull : ((1ull << t.n) - 1));
   bool zeroed = false;  // states zeroed before the first pass (the skipped items hold zeros)
+  uint64_t proj_next = 0;  // qubits the last region's unguarded measure / reset ops project
   for (size_t si = 0; si < P.steps.size(); ++si) {
     const Step& s = P.steps[si];
     if (s.type == 0) {
@@ -366,7 +367,14 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
           ++j;
         }
       }
-      const double pass_frac = std::ldexp(1.0, -__builtin_popcountll(pd.zero_tid));  // executed share of the flops
+      const double pass_frac = std::ldexp(1.0, -__builtin_popcountll(pd.zero_tid));  // share of the items run
+      // the first pass after a measurement: items whose out-of-tile bits the collapse
+      // rejects only store zeros (pass driver, PassItem::zero); the qubits every live
+      // trajectory projects give the executed share (accounting only)
+      const double read_frac = (pd.prologue && a.phases && pd.rb > 0 && !pd.epi)
+                                   ? std::ldexp(1.0, -__builtin_popcountll(proj_next & ~pd.smask))
+                                   : 1.0;
+      proj_next = 0;
       for (int g = pd.gate_begin; g < pd.gate_begin + pd.gate_count; ++g) {  // qubits this pass can move
         const PassGate& q = P.gates[g];
         if (q.gclass == GC_DIAG || q.gclass == GC_DIAG_GLOBAL) continue;
@@ -397,11 +405,12 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
         QSB_CUDA(launch(a));
       }
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
-      r.pass_bytes += (pd.init_zero ? 1.0 : 2.0) * state_bytes;
-      ctx->run_flops += r.pd->pflops[s.index] * pass_frac * (double)r.slots;
+      const double byte_frac = pass_frac * (pd.init_zero ? 1.0 : 1.0 + read_frac);  // writes + reads
+      r.pass_bytes += byte_frac * state_bytes;
+      ctx->run_flops += r.pd->pflops[s.index] * pass_frac * read_frac * (double)r.slots;
       if (dedup) {  // the kernels touched only the representatives
-        launch_accum_physical(d_nactive, r.pd->pflops[s.index] * pass_frac,
-                              (pd.init_zero ? 1.0 : 2.0) * state_bytes / (double)r.slots, d_phys, ctx->stream);
+        launch_accum_physical(d_nactive, r.pd->pflops[s.index] * pass_frac * read_frac,
+                              byte_frac * state_bytes / (double)r.slots, d_phys, ctx->stream);
         r.launches++;
       }
       r.passes++;
@@ -425,6 +434,10 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
       acc = 0;
       consumed = 0;
       if (rd.op_end > rd.op_begin) untouched = 0;  // after a measurement: no known-zero qubits
+      for (int oi = rd.op_begin; oi < rd.op_end; ++oi) {
+        const DevOp& op = P.region_ops[oi];
+        if ((op.kind == QSB_OP_MEASURE || op.kind == QSB_OP_RESET) && op.guard < 0) proj_next |= 1ull << op.qubit;
+      }
     }
   }
   r.final_clear = acc;

@@ -58,6 +58,7 @@ template <typename R> struct PassCtx {
 struct PassItem {
   int64_t slot;
   int64_t src;  // slot whose buffer the gather reads (history dedup: a branch's first pass)
+  bool zero;    // the pending projection zeroes the whole item: no gather, no gates, zeros stored
   uint64_t base_phys, base_log, Kp, Vp;
   uint32_t fl;
   bool alive, pending;
@@ -145,6 +146,9 @@ __device__ __forceinline__ PassItem item_of(const SlotCtx& s, const PassDesc& pd
   it.sre = s.sre;
   it.sim = s.sim;
   it.base_phys = tab64(tb.pdt, tile, ntl);
+  // the collapse of the previous measurement keeps only (p & Kp) == Vp: when the item's
+  // out-of-tile bits already disagree, every amplitude of it becomes zero
+  it.zero = s.pending && ((it.base_phys ^ s.Vp) & s.Kp & ~pd.smask) != 0 && !pd.epi;
   it.base_log = it.base_phys ^ (s.F & ~pd.smask);
   it.fl = tab32(tb.pxs, s.F, n);
   return it;
@@ -292,7 +296,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   };
 
   auto prefetch = [&](const PassItem& it, A* dst) {
-    if (!it.alive) return;
+    if (!it.alive || it.zero) return;
     const A* st = reinterpret_cast<const A*>(a.state) + (it.src << a.n);
     const uint64_t pb = it.base_phys | Pt;
     const uint32_t fb = flip_base(it.fl);
@@ -469,7 +473,7 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
         if (wn < W) prefetch(cur, bufs);
         cp_async_commit();
       };
-      if (it.alive) {
+      if (it.alive && !it.zero) {
         A dummy[1];
         process(it, bufs, dummy);
         PassCtx<R> cx{bufs, sg, swz, tid, T, TL, bar};
@@ -477,11 +481,22 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
         run_last(cx, dst, hi_off, mid);
       } else {
         mid();
+        if (it.alive) {  // projected away: store zeros
+          A z[1 << RB];
+#pragma unroll
+          for (int j = 0; j < (1 << RB); ++j) z[j] = mk<R>((R)0, (R)0);
+          scatter(it, z);
+        }
       }
       continue;
     }
     A v[1 << RB];
-    if (it.alive) process(it, bufs + b * TL, v);
+    if (it.alive && !it.zero) {
+      process(it, bufs + b * TL, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < (1 << RB); ++j) v[j] = mk<R>((R)0, (R)0);
+    }
     // single buffer: the tile is in registers -- release the buffer, start the next
     // item's gather, then store, so that the scatter and the next gather overlap
     __syncthreads();
