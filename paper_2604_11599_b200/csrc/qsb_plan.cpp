@@ -266,6 +266,10 @@ struct Planner {
   bool phase_search_ = P.opt.phase_search != 0;
   bool block_condx_ = P.opt.block_condx != 0;
   int defer_from_ = P.opt.defer_gates;  // 0: off; r: defer past measurement regions r, r+1, ...
+  // qubits every trajectory projected in the measurement region just closed (unguarded
+  // measure / reset): the next region's first pass runs only the items whose out-of-tile
+  // projected bits match (the others store zeros) -- its tile set may avoid them
+  uint64_t zero_next_ = 0;
   std::vector<RegionBuild> regions;
 
   Planner(const TapeInfo& t_, int k_, int lowq_, int rb_, StreamPlan& p) : t(t_), k(k_), lowq(lowq_), rb(rb_), P(p) {}
@@ -527,7 +531,7 @@ struct Planner {
   // its targets are in S (diagonal gates anywhere) and no earlier rejected gate shares a
   // qubit with it; grow = true lets S grow (greedy first fit) up to k qubits
   int absorb(const std::vector<int>& remaining, uint64_t& S, bool grow, std::vector<int>* chosen,
-             std::vector<int>* rest) const {
+             std::vector<int>* rest, uint64_t forbid = 0) const {
     uint64_t blocked = 0;
     int taken = 0;
     for (int gi : remaining) {
@@ -544,7 +548,7 @@ struct Planner {
         continue;
       }
       const uint64_t need = d.gclass == GC_DIAG ? 0 : (tm & ~S);
-      if (!need || (grow && popc(S | need) <= k)) {
+      if (!need || (grow && popc(S | need) <= k && !(need & forbid))) {
         S |= need;
         if (chosen) chosen->push_back(gi);
         ++taken;
@@ -575,14 +579,11 @@ struct Planner {
     return c;
   }
 
-  // one gate region -> passes, by a beam search over the tile set of each pass (kBeam
+  // tile sets of the passes of `buf` by a beam search over the tile set of each pass (kBeam
   // partial schedules, kCand tile sets tried per step, ranked by the gates still left):
   // the fewest passes found -- each pass is a full read + write of every state
-  void flush(std::vector<int>& buf, int epi_region) {
-    if (buf.empty()) {
-      if (epi_region >= 0) emit_pass(low_mask(), {}, epi_region);
-      return;
-    }
+  std::vector<uint64_t> beam_sets(const std::vector<int>& buf) const {
+    if (buf.empty()) return {};
     // beam width scaled to the region so planning stays ~linear in the gate count (64 x 16
     // up to ~6k gates per region: DYN20 / RDC / VQE; a 100k-gate static region gets 4 x 8)
     const int kBeam = (int)std::max<size_t>(4, std::min<size_t>(64, 400000 / std::max<size_t>(1, buf.size())));
@@ -592,9 +593,7 @@ struct Planner {
       std::vector<int> remaining;
     };
     std::vector<Sched> beam{Sched{{}, buf}};
-    Sched done;
-    bool found = false;
-    while (!found) {
+    while (true) {
       std::vector<Sched> next;
       for (const Sched& st : beam) {
         auto cands = candidates(st.remaining);
@@ -603,28 +602,71 @@ struct Planner {
           ns.sets = st.sets;
           uint64_t S = cands[ci].second;
           std::vector<int> chosen;
-          absorb(st.remaining, S, false, &chosen,
-                 &ns.remaining);
+          absorb(st.remaining, S, false, &chosen, &ns.remaining);
           if (chosen.empty()) continue;
           ns.sets.push_back(S);
           next.push_back(std::move(ns));
         }
       }
-      if (next.empty()) break;  // cannot happen: the first gate of a region always fits
+      if (next.empty()) return {};  // cannot happen: the first gate of a region always fits
       std::stable_sort(next.begin(), next.end(),
                        [](const Sched& a, const Sched& b) { return a.remaining.size() < b.remaining.size(); });
-      if (next[0].remaining.empty()) {
-        done = std::move(next[0]);
-        found = true;
-        break;
-      }
+      if (next[0].remaining.empty()) return next[0].sets;
       if ((int)next.size() > kBeam) next.resize(kBeam);
       beam.swap(next);
     }
+  }
+
+  // relative cost of a region's schedule: 1 per pass, except a first pass after a
+  // measurement whose tile leaves u projected qubits outside (2^-u of its items run, the
+  // others store zeros: ~0.15 of a pass) -- and not when it is the epilogue pass
+  double sched_cost(const std::vector<uint64_t>& sets, uint64_t Z) const {
+    double c = (double)sets.size();
+    if (Z && sets.size() > 1) {
+      const double f = std::ldexp(1.0, -popc(Z & ~sets[0]));
+      c -= 1.0 - (f + 0.15 * (1.0 - f));
+    }
+    return c;
+  }
+
+  void flush(std::vector<int>& buf, int epi_region) {
+    const uint64_t Z = zero_next_;
+    zero_next_ = 0;
+    if (buf.empty()) {
+      if (epi_region >= 0) emit_pass(low_mask(), {}, epi_region);
+      return;
+    }
+    std::vector<uint64_t> sets = beam_sets(buf);
+    // after a measurement: also try a first pass whose tile avoids the projected qubits
+    // (above the always-present low run), the rest by the beam search; keep the cheaper
+    const uint64_t avoid = Z & ~low_mask();
+    if (P.opt.zero_aware && avoid) {
+      std::vector<std::pair<int, uint64_t>> c1;
+      uint64_t g = low_mask();
+      c1.push_back({absorb(buf, g, true, nullptr, nullptr, avoid), g});
+      const int w = k - lowq;
+      for (int a = lowq; w > 0 && a + w <= t.n; ++a) {
+        uint64_t S = low_mask() | (((w >= 64) ? ~0ull : ((1ull << w) - 1)) << a);
+        if (S & avoid) continue;
+        c1.push_back({absorb(buf, S, false, nullptr, nullptr), S});
+      }
+      std::stable_sort(c1.begin(), c1.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (size_t ci = 0; ci < c1.size() && ci < 4; ++ci) {
+        if (c1[ci].first == 0) break;
+        uint64_t S1 = c1[ci].second;
+        std::vector<int> chosen, rest;
+        absorb(buf, S1, false, &chosen, &rest);
+        std::vector<uint64_t> alt{S1};
+        const std::vector<uint64_t> tail = beam_sets(rest);
+        if (!rest.empty() && tail.empty()) continue;
+        alt.insert(alt.end(), tail.begin(), tail.end());
+        if (sched_cost(alt, Z) < sched_cost(sets, Z) - 1e-9) sets = alt;
+      }
+    }
     // replay the chosen tile sets
     std::vector<int> remaining = buf;
-    for (size_t i = 0; i < done.sets.size(); ++i) {
-      uint64_t S = done.sets[i];
+    for (size_t i = 0; i < sets.size(); ++i) {
+      uint64_t S = sets[i];
       std::vector<int> chosen, rest;
       absorb(remaining, S, false, &chosen, &rest);
       emit_pass(S, chosen, rest.empty() ? epi_region : -1);
@@ -692,6 +734,9 @@ struct Planner {
       split_deferred(pre, M, defer_from_ > 0 && open_region >= defer_from_, kept, deferred);
       flush(kept, open_region);
       P.steps.push_back({1, open_region});
+      zero_next_ = 0;
+      for (const DevOp& d : R.ops)
+        if ((d.kind == QSB_OP_MEASURE || d.kind == QSB_OP_RESET) && d.guard < 0) zero_next_ |= 1ull << d.qubit;
       // deferred gates run first in the next gate region (relative order kept)
       deferred.insert(deferred.end(), buf.begin(), buf.end());
       buf.swap(deferred);
@@ -856,6 +901,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "edge_x") edge_x = v;
   else if (key == "ctas_per_sm") ctas_per_sm = v;
   else if (key == "defer_gates") defer_gates = v;
+  else if (key == "zero_aware") zero_aware = v;
   else return false;
   return true;
 }
