@@ -367,11 +367,25 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
           ++j;
         }
       }
+      // The first pass after a measurement: the amplitudes the pending collapse rejects on
+      // the out-of-tile qubits every live trajectory projected (the region's unguarded
+      // measure / reset ops) are zero-filled by a streaming kernel, and the pass runs only
+      // the items the collapse keeps (tile-id bits fixed to the slot's projection values).
+      // (Items rejected on other qubits take the per-item zero-store path, PassItem::zero.)
+      uint64_t proj_out = 0;
+      if (pd.prologue && a.phases && pd.rb > 0 && !pd.epi && ctx->opt_zero_fill) {
+        proj_out = proj_next & ~pd.smask & ~1ull;  // (qubit 0 is always in the tile's low run)
+        int j = 0;
+        for (int q = 0; q < t.n; ++q) {
+          if (pd.smask >> q & 1) continue;
+          if (proj_out >> q & 1) pd.zero_tid |= 1ull << j;
+          ++j;
+        }
+        pd.zero_from_vp = proj_out ? 1 : 0;
+      }
       const double pass_frac = std::ldexp(1.0, -__builtin_popcountll(pd.zero_tid));  // share of the items run
-      // the first pass after a measurement: items whose out-of-tile bits the collapse
-      // rejects only store zeros (pass driver, PassItem::zero); the qubits every live
-      // trajectory projects give the executed share (accounting only)
-      const double read_frac = (pd.prologue && a.phases && pd.rb > 0 && !pd.epi)
+      // per-item zero stores (no zero fill): the executed share, for the accounting only
+      const double read_frac = (!proj_out && pd.prologue && a.phases && pd.rb > 0 && !pd.epi)
                                    ? std::ldexp(1.0, -__builtin_popcountll(proj_next & ~pd.smask))
                                    : 1.0;
       proj_next = 0;
@@ -394,18 +408,25 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
         b.active = d_split;
         b.nactive = d_split + 2 * r.slots;
         b.read_src = d_copy_src;
+        if (proj_out) launch_zero_projected(b, r.c64, proj_out, ctx->stream);  // own buffers
         QSB_CUDA(launch(b));
         b.active = d_split + r.slots;
         b.nactive = d_split + 2 * r.slots + 1;
         b.read_src = nullptr;
+        if (proj_out) launch_zero_projected(b, r.c64, proj_out, ctx->stream);  // after the branches read them
         QSB_CUDA(launch(b));
-        r.launches++;
+        r.launches += proj_out ? 3 : 1;
         split_next = false;
       } else {
+        if (proj_out) {
+          launch_zero_projected(a, r.c64, proj_out, ctx->stream);
+          r.launches++;
+        }
         QSB_CUDA(launch(a));
       }
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
-      const double byte_frac = pass_frac * (pd.init_zero ? 1.0 : 1.0 + read_frac);  // writes + reads
+      // writes + reads of the items run (+ the zero fill's writes of the others)
+      const double byte_frac = pass_frac * (pd.init_zero ? 1.0 : 1.0 + read_frac) + (proj_out ? 1.0 - pass_frac : 0.0);
       r.pass_bytes += byte_frac * state_bytes;
       ctx->run_flops += r.pd->pflops[s.index] * pass_frac * read_frac * (double)r.slots;
       if (dedup) {  // the kernels touched only the representatives
@@ -589,7 +610,8 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
   else if (k == "jit_async") ctx->opt_jit_async = value;
-  else if (k == "defer_copy") ctx->opt_defer_copy = value;  // dedup: branches read the old buffer in their first pass  // NVRTC in the background, generic kernel meanwhile
+  else if (k == "defer_copy") ctx->opt_defer_copy = value;
+  else if (k == "zero_fill") ctx->opt_zero_fill = value;  // first pass after a measurement: zero fill + kept items only  // dedup: branches read the old buffer in their first pass  // NVRTC in the background, generic kernel meanwhile
   else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles
   else if (k == "expval_jit") ctx->opt_ev_jit = value;          // NVRTC-specialised Pauli reducer
   else if (k == "expval_jit_terms") ctx->opt_ev_jit_terms = value;  // its terms per launch (<= 32)

@@ -144,6 +144,11 @@ struct PassDesc {
   // start; set by the host per run): every item with one of them set is zero before and
   // after the pass and its buffer already holds zeros -- only the others run
   uint64_t zero_tid;
+  // 1: the known bits of zero_tid are the slot's projection values (first pass after a
+  // measurement: the rejected items were zero-filled by the host's k_zero_projected), 0:
+  // they are 0 (|0...0> start)
+  int32_t zero_from_vp;
+  int32_t pad_z;
 };
 
 struct RegionDesc {

@@ -68,7 +68,7 @@ struct qsb_ctx_s {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<cudaEvent_t> pass_events;
   int64_t opt_tile = 0, opt_batch = 0, opt_resident_max = -1, opt_engine = -1, opt_jit = 1, opt_jit_min = 13;
-  int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1, opt_lowq = 0, opt_jit_async = 0, opt_ev_lowq = 0, opt_ev_jit = 1, opt_ev_jit_terms = 32, opt_defer_copy = 1;
+  int64_t opt_dedup = 1, opt_reg_bits = 4, opt_fuse = 1, opt_lowq = 0, opt_jit_async = 0, opt_ev_lowq = 0, opt_ev_jit = 1, opt_ev_jit_terms = 32, opt_defer_copy = 1, opt_zero_fill = 1;
   qsb::EngineOptions eopt;  // planner / NVRTC generator options (qsb_plan.h)
   DevBuf state, partial, ctl, bits, guards, mats, params, predrawn, status, counters, misc, misc2, trace, dedup;
   DevBuf shotwords, histo;  // device-side shot histogram (qsb_sample_counts)

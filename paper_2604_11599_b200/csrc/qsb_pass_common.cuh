@@ -286,8 +286,10 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
   const int64_t W = (int64_t)(a.active ? *a.nactive : a.slots) << ntl_run;
   auto item_at = [&](int64_t w) -> PassItem {
     if (!pd.zero_tid) return pass_item(a, pd, w, ntl, itb);
-    const uint64_t tile = pdep64((uint64_t)w & ((1ull << ntl_run) - 1), tid_free);
-    return item_of(slot_ctx(a, pd, w >> ntl_run), pd, tile, ntl, a.n, itb);
+    const SlotCtx sc = slot_ctx(a, pd, w >> ntl_run);
+    uint64_t tile = pdep64((uint64_t)w & ((1ull << ntl_run) - 1), tid_free);
+    if (pd.zero_from_vp) tile |= tab64(itb.pxo, sc.Vp, a.n) & pd.zero_tid;  // the items the collapse keeps
+    return item_of(sc, pd, tile, ntl, a.n, itb);
   };
 
   // swizzled-slot base of this thread for an item with frame flip fl

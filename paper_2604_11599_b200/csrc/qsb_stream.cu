@@ -576,6 +576,30 @@ __global__ void k_zero_slots(StreamArgs a, int64_t amp_words, int zero_partials)
   }
 }
 
+// the amplitudes the pending collapse rejects on the (out-of-tile) qubits M, per active
+// slot: zero stores, so that the next pass runs only the items the collapse keeps
+__global__ void k_zero_projected(StreamArgs a, uint64_t M, int64_t amp_words, int amps_per_word) {
+  const int64_t n_act = a.active ? *a.nactive : a.slots;
+  for (int64_t si = blockIdx.y; si < n_act; si += gridDim.y) {
+    const int64_t slot = a.active ? a.active[si] : si;
+    const TrajCtl& c = a.ctl[slot];
+    if (c.status != 0 || !c.pending) continue;
+    const uint64_t V = c.kval & M;
+    int4* st = reinterpret_cast<int4*>(a.state) + slot * amp_words;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < amp_words; i += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t p = (uint64_t)i * (uint64_t)amps_per_word;  // M never holds bit 0 (low run in the tile)
+      if ((p & M) != V) st[i] = make_int4(0, 0, 0, 0);
+    }
+  }
+}
+
+void launch_zero_projected(const StreamArgs& a, int c64, uint64_t M, cudaStream_t s) {
+  const int64_t words = ((int64_t)(c64 ? 8 : 16) << a.n) / 16;
+  const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 1024), 64);
+  const unsigned gy = (unsigned)std::min<int64_t>(a.slots, 65535);
+  k_zero_projected<<<dim3(gx, gy), 256, 0, s>>>(a, M, words, c64 ? 2 : 1);
+}
+
 void launch_zero_slots(const StreamArgs& a, int c64, int zero_partials, cudaStream_t s) {
   const int64_t words = ((int64_t)(c64 ? 8 : 16) << a.n) / 16;
   const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, words / 1024), 64);
