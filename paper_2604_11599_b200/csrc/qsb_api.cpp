@@ -339,6 +339,7 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
   uint64_t untouched = r.in_place ? 0 : ((t.n >= 64) ? ~0ull : ((1ull << t.n) - 1));
   bool zeroed = false;  // states zeroed before the first pass (the skipped items hold zeros)
   uint64_t proj_next = 0;  // qubits the last region's unguarded measure / reset ops project
+  uint64_t zero_known = 0; // projected qubits whose rejected amplitudes no pass has stored yet
   for (size_t si = 0; si < P.steps.size(); ++si) {
     const Step& s = P.steps[si];
     if (s.type == 0) {
@@ -367,27 +368,39 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
           ++j;
         }
       }
-      // The first pass after a measurement: the amplitudes the pending collapse rejects on
-      // the out-of-tile qubits every live trajectory projected (the region's unguarded
-      // measure / reset ops) are zero-filled by a streaming kernel, and the pass runs only
-      // the items the collapse keeps (tile-id bits fixed to the slot's projection values).
-      // (Items rejected on other qubits take the per-item zero-store path, PassItem::zero.)
-      uint64_t proj_out = 0;
-      if (pd.prologue && a.phases && pd.rb > 0 && !pd.epi && ctx->opt_zero_fill) {
-        proj_out = proj_next & ~pd.smask & ~1ull;  // (qubit 0 is always in the tile's low run)
+      // After a measurement, the amplitudes the collapse rejects on the qubits every live
+      // trajectory projected (the region's unguarded measure / reset ops) are zero.  The
+      // first pass runs only the items the collapse keeps on its out-of-tile qubits (tile-
+      // id bits fixed to the slot's projection values) and stores nothing for the others;
+      // those qubits stay "known zero" (zero_known) until a pass holds them in its tile:
+      // its gather makes the rejected amplitudes zero instead of reading the stale buffer,
+      // and it skips the items rejected on its own out-of-tile known-zero qubits.
+      // (Items rejected on qubits some trajectories did not project take the per-item
+      // zero-store path, PassItem::zero.)
+      const bool driver = a.phases && pd.rb > 0;
+      uint64_t zo = 0;  // known-zero qubits outside this pass's tile whose rejected items it skips
+      pd.zk_mask = 0;
+      if (driver && ctx->opt_zero_fill) {
+        if (pd.prologue && !pd.epi) zero_known = proj_next & ~pd.smask & ~1ull;  // (qubit 0: always in the low run)
+        if (!pd.prologue) pd.zk_mask = zero_known;
+        zo = pd.epi ? 0 : (zero_known & ~pd.smask);
         int j = 0;
         for (int q = 0; q < t.n; ++q) {
           if (pd.smask >> q & 1) continue;
-          if (proj_out >> q & 1) pd.zero_tid |= 1ull << j;
+          if (zo >> q & 1) pd.zero_tid |= 1ull << j;
           ++j;
         }
-        pd.zero_from_vp = proj_out ? 1 : 0;
+        pd.zero_from_vp = zo ? 1 : 0;
+      } else if (zero_known) {  // a pass that reads every amplitude: store the zeros first
+        launch_zero_projected(a, r.c64, zero_known, ctx->stream);
+        r.launches++;
+        zero_known = 0;
       }
       const double pass_frac = std::ldexp(1.0, -__builtin_popcountll(pd.zero_tid));  // share of the items run
-      // per-item zero stores (no zero fill): the executed share, for the accounting only
-      const double read_frac = (!proj_out && pd.prologue && a.phases && pd.rb > 0 && !pd.epi)
-                                   ? std::ldexp(1.0, -__builtin_popcountll(proj_next & ~pd.smask))
-                                   : 1.0;
+      // per-item zero stores: the executed share, for the accounting only
+      const bool item_zero = !zo && pd.prologue && driver && !pd.epi;  // per-item zero stores only
+      const double flop_frac = item_zero ? std::ldexp(1.0, -__builtin_popcountll(proj_next & ~pd.smask)) : 1.0;
+      const double read_frac = flop_frac * std::ldexp(1.0, -__builtin_popcountll(pd.zk_mask & pd.smask));
       proj_next = 0;
       for (int g = pd.gate_begin; g < pd.gate_begin + pd.gate_count; ++g) {  // qubits this pass can move
         const PassGate& q = P.gates[g];
@@ -408,29 +421,27 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
         b.active = d_split;
         b.nactive = d_split + 2 * r.slots;
         b.read_src = d_copy_src;
-        if (proj_out) launch_zero_projected(b, r.c64, proj_out, ctx->stream);  // own buffers
         QSB_CUDA(launch(b));
         b.active = d_split + r.slots;
         b.nactive = d_split + 2 * r.slots + 1;
         b.read_src = nullptr;
-        if (proj_out) launch_zero_projected(b, r.c64, proj_out, ctx->stream);  // after the branches read them
         QSB_CUDA(launch(b));
-        r.launches += proj_out ? 3 : 1;
+        r.launches++;
         split_next = false;
       } else {
-        if (proj_out) {
-          launch_zero_projected(a, r.c64, proj_out, ctx->stream);
-          r.launches++;
-        }
         QSB_CUDA(launch(a));
       }
       cudaEventRecord(ctx->pass_events[2 * s.index + 1], ctx->stream);
-      // writes + reads of the items run (+ the zero fill's writes of the others)
-      const double byte_frac = pass_frac * (pd.init_zero ? 1.0 : 1.0 + read_frac) + (proj_out ? 1.0 - pass_frac : 0.0);
+      // the pass stored every amplitude of its items: its tile qubits are materialised; with
+      // no item skipped, all of them
+      zero_known = pd.zero_tid ? (zero_known & ~pd.smask) : 0;
+      if (!driver) zero_known = 0;
+      // writes + reads of the items run
+      const double byte_frac = pass_frac * (pd.init_zero ? 1.0 : 1.0 + read_frac);
       r.pass_bytes += byte_frac * state_bytes;
-      ctx->run_flops += r.pd->pflops[s.index] * pass_frac * read_frac * (double)r.slots;
+      ctx->run_flops += r.pd->pflops[s.index] * pass_frac * flop_frac * (double)r.slots;
       if (dedup) {  // the kernels touched only the representatives
-        launch_accum_physical(d_nactive, r.pd->pflops[s.index] * pass_frac * read_frac,
+        launch_accum_physical(d_nactive, r.pd->pflops[s.index] * pass_frac * flop_frac,
                               byte_frac * state_bytes / (double)r.slots, d_phys, ctx->stream);
         r.launches++;
       }
@@ -460,6 +471,10 @@ int run_stream(qsb_ctx ctx, StreamRun& r) {
         if ((op.kind == QSB_OP_MEASURE || op.kind == QSB_OP_RESET) && op.guard < 0) proj_next |= 1ull << op.qubit;
       }
     }
+  }
+  if (zero_known) {  // the run ends with rejected amplitudes never stored: store the zeros
+    launch_zero_projected(a, r.c64, zero_known, ctx->stream);
+    r.launches++;
   }
   r.final_clear = acc;
   r.final_consumed = consumed;

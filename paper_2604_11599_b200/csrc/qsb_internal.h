@@ -144,11 +144,14 @@ struct PassDesc {
   // start; set by the host per run): every item with one of them set is zero before and
   // after the pass and its buffer already holds zeros -- only the others run
   uint64_t zero_tid;
-  // 1: the known bits of zero_tid are the slot's projection values (first pass after a
-  // measurement: the rejected items were zero-filled by the host's k_zero_projected), 0:
-  // they are 0 (|0...0> start)
+  // 1: the known bits of zero_tid are the slot's projection values (after a measurement:
+  // the items the collapse rejects are zero but not stored), 0: they are 0 (|0...0> start)
   int32_t zero_from_vp;
   int32_t pad_z;
+  // qubits whose amplitudes the last collapse rejected (p & zk_mask != kval & zk_mask) and
+  // that no pass has stored since: the gather makes those amplitudes zero instead of
+  // reading them (the buffer still holds stale values there)
+  uint64_t zk_mask;
 };
 
 struct RegionDesc {

@@ -308,6 +308,8 @@ __device__ __forceinline__ void pass_persistent(const StreamArgs& a, const PassD
       const uint64_t p = pb | hi_off[j * hstep];
       if (pd.init_zero) {
         *d = mk<R>(p == 0 ? (R)1 : (R)0, (R)0);
+      } else if (((p ^ it.Vp) & pd.zk_mask) != 0) {  // rejected by the last collapse, never stored since
+        *d = mk<R>((R)0, (R)0);
       } else if (sizeof(A) == 16) {
         cp_async16(d, st + p);
       } else {
