@@ -617,16 +617,34 @@ struct Planner {
     }
   }
 
-  // relative cost of a region's schedule: 1 per pass, except a first pass after a
-  // measurement whose tile leaves u projected qubits outside (2^-u of its items run, the
-  // others store zeros: ~0.15 of a pass) -- and not when it is the epilogue pass
+  // relative cost of a region's schedule: 1 per pass, except the passes after a
+  // measurement while projected qubits Z have not been in a tile yet: a pass that leaves u
+  // of them outside runs 2^-u of its items (the rejected ones are neither read nor stored;
+  // §4.2) -- not for the region's epilogue pass (its marginal needs every item)
   double sched_cost(const std::vector<uint64_t>& sets, uint64_t Z) const {
-    double c = (double)sets.size();
-    if (Z && sets.size() > 1) {
-      const double f = std::ldexp(1.0, -popc(Z & ~sets[0]));
-      c -= 1.0 - (f + 0.15 * (1.0 - f));
+    double c = 0;
+    for (size_t i = 0; i < sets.size(); ++i) {
+      const bool epi = i + 1 == sets.size();
+      c += (Z && !epi) ? std::ldexp(1.0, -popc(Z & ~sets[i])) : 1.0;
+      Z &= ~sets[i];
     }
     return c;
+  }
+
+  // tile sets that avoid the qubits `avoid` (above the low run): the greedy first-fit set
+  // with them forbidden and the windows without them, ranked by the gates they absorb
+  std::vector<std::pair<int, uint64_t>> avoiding(const std::vector<int>& remaining, uint64_t avoid) const {
+    std::vector<std::pair<int, uint64_t>> c1;
+    uint64_t g = low_mask();
+    c1.push_back({absorb(remaining, g, true, nullptr, nullptr, avoid), g});
+    const int w = k - lowq;
+    for (int a = lowq; w > 0 && a + w <= t.n; ++a) {
+      uint64_t S = low_mask() | (((w >= 64) ? ~0ull : ((1ull << w) - 1)) << a);
+      if (S & avoid) continue;
+      c1.push_back({absorb(remaining, S, false, nullptr, nullptr), S});
+    }
+    std::stable_sort(c1.begin(), c1.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    return c1;
   }
 
   void flush(std::vector<int>& buf, int epi_region) {
@@ -637,30 +655,46 @@ struct Planner {
       return;
     }
     std::vector<uint64_t> sets = beam_sets(buf);
-    // after a measurement: also try a first pass whose tile avoids the projected qubits
-    // (above the always-present low run), the rest by the beam search; keep the cheaper
+    // after a measurement: also try one or two first passes whose tiles avoid the projected
+    // qubits (above the always-present low run), the rest by the beam search; keep the
+    // cheapest schedule
     const uint64_t avoid = Z & ~low_mask();
-    if (P.opt.zero_aware && avoid) {
-      std::vector<std::pair<int, uint64_t>> c1;
-      uint64_t g = low_mask();
-      c1.push_back({absorb(buf, g, true, nullptr, nullptr, avoid), g});
-      const int w = k - lowq;
-      for (int a = lowq; w > 0 && a + w <= t.n; ++a) {
-        uint64_t S = low_mask() | (((w >= 64) ? ~0ull : ((1ull << w) - 1)) << a);
-        if (S & avoid) continue;
-        c1.push_back({absorb(buf, S, false, nullptr, nullptr), S});
+    if (P.opt.zero_aware && avoid && buf.size() <= 4000) {
+      double best = sched_cost(sets, Z);
+      std::vector<std::vector<uint64_t>> prefixes;
+      for (const auto& c1 : avoiding(buf, avoid)) {
+        if (c1.first == 0 || prefixes.size() >= 4) break;
+        prefixes.push_back({c1.second});
       }
-      std::stable_sort(c1.begin(), c1.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-      for (size_t ci = 0; ci < c1.size() && ci < 4; ++ci) {
-        if (c1[ci].first == 0) break;
-        uint64_t S1 = c1[ci].second;
-        std::vector<int> chosen, rest;
-        absorb(buf, S1, false, &chosen, &rest);
-        std::vector<uint64_t> alt{S1};
-        const std::vector<uint64_t> tail = beam_sets(rest);
-        if (!rest.empty() && tail.empty()) continue;
+      const size_t n1 = prefixes.size();
+      if (P.opt.zero_aware >= 2)
+        for (size_t i = 0; i < n1; ++i) {  // a second avoiding pass after each first one
+          uint64_t S1 = prefixes[i][0];
+          std::vector<int> chosen, rest;
+          absorb(buf, S1, false, &chosen, &rest);
+          int taken = 0;
+          for (const auto& c2 : avoiding(rest, avoid)) {
+            if (c2.first == 0 || taken >= 2) break;
+            prefixes.push_back({S1, c2.second});
+            ++taken;
+          }
+        }
+      for (const auto& pre : prefixes) {
+        std::vector<int> remaining = buf;
+        for (uint64_t S : pre) {
+          std::vector<int> chosen, rest;
+          absorb(remaining, S, false, &chosen, &rest);
+          remaining.swap(rest);
+        }
+        std::vector<uint64_t> alt = pre;
+        const std::vector<uint64_t> tail = beam_sets(remaining);
+        if (!remaining.empty() && tail.empty()) continue;
         alt.insert(alt.end(), tail.begin(), tail.end());
-        if (sched_cost(alt, Z) < sched_cost(sets, Z) - 1e-9) sets = alt;
+        const double c = sched_cost(alt, Z);
+        if (c < best - 1e-9) {
+          best = c;
+          sets = alt;
+        }
       }
     }
     // replay the chosen tile sets

@@ -54,7 +54,7 @@ struct EngineOptions {
   int edge_x = 1;             // conditional X gates at a phase edge as slot-base XORs
   int ctas_per_sm = 0;        // cap of the persistent pass grid per SM (0: occupancy)
   int defer_gates = 0;        // gates commuting with a measurement region run after it (measured slower: off)
-  int zero_aware = 1;         // the first pass after a measurement may avoid the projected qubits
+  int zero_aware = 2;         // after a measurement, the first (1) or first two (2) passes may avoid the projected qubits
   uint64_t key() const {
     const int v[] = {pair_aware, phase_search, block_condx, inline_phases, inline_min_gates, ffma2, packed_gates,
                      last_direct, last_direct_maxlow, minblocks, edge_x, ctas_per_sm, defer_gates, inline_max_phases,
