@@ -666,19 +666,28 @@ struct Planner {
         if (c1.first == 0 || prefixes.size() >= 4) break;
         prefixes.push_back({c1.second});
       }
-      const size_t n1 = prefixes.size();
-      if (P.opt.zero_aware >= 2)
-        for (size_t i = 0; i < n1; ++i) {  // a second avoiding pass after each first one
-          uint64_t S1 = prefixes[i][0];
-          std::vector<int> chosen, rest;
-          absorb(buf, S1, false, &chosen, &rest);
+      // deeper prefixes: after each prefix, up to two more avoiding passes (zero_aware =
+      // the most avoiding passes per region)
+      for (size_t lo = 0, depth = 2; depth <= (size_t)P.opt.zero_aware; ++depth) {
+        const size_t hi = prefixes.size();
+        for (size_t i = lo; i < hi; ++i) {
+          std::vector<int> remaining = buf;
+          for (uint64_t S : prefixes[i]) {
+            std::vector<int> chosen, rest;
+            absorb(remaining, S, false, &chosen, &rest);
+            remaining.swap(rest);
+          }
           int taken = 0;
-          for (const auto& c2 : avoiding(rest, avoid)) {
+          for (const auto& c2 : avoiding(remaining, avoid)) {
             if (c2.first == 0 || taken >= 2) break;
-            prefixes.push_back({S1, c2.second});
+            std::vector<uint64_t> pre = prefixes[i];
+            pre.push_back(c2.second);
+            prefixes.push_back(pre);
             ++taken;
           }
         }
+        lo = hi;
+      }
       for (const auto& pre : prefixes) {
         std::vector<int> remaining = buf;
         for (uint64_t S : pre) {
