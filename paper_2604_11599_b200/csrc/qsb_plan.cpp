@@ -621,11 +621,23 @@ struct Planner {
   // measurement while projected qubits Z have not been in a tile yet: a pass that leaves u
   // of them outside runs 2^-u of its items (the rejected ones are neither read nor stored;
   // §4.2) -- not for the region's epilogue pass (its marginal needs every item)
-  double sched_cost(const std::vector<uint64_t>& sets, uint64_t Z) const {
+  // (zero_cost = 1: a pass weighs max(0.45, gates / 70) -- the memory floor of a pass
+  // against the compute of a ~70-gate DYN20 pass -- instead of 1)
+  double sched_cost(const std::vector<uint64_t>& sets, uint64_t Z, const std::vector<int>* buf = nullptr) const {
     double c = 0;
+    std::vector<int> remaining;
+    if (buf) remaining = *buf;
     for (size_t i = 0; i < sets.size(); ++i) {
       const bool epi = i + 1 == sets.size();
-      c += (Z && !epi) ? std::ldexp(1.0, -popc(Z & ~sets[i])) : 1.0;
+      double w = 1.0;
+      if (buf && P.opt.zero_cost) {
+        uint64_t S = sets[i];
+        std::vector<int> chosen, rest;
+        absorb(remaining, S, false, &chosen, &rest);
+        remaining.swap(rest);
+        w = std::max(0.45, (double)chosen.size() / 70.0);
+      }
+      c += w * ((Z && !epi) ? std::ldexp(1.0, -popc(Z & ~sets[i])) : 1.0);
       Z &= ~sets[i];
     }
     return c;
@@ -660,7 +672,7 @@ struct Planner {
     // cheapest schedule
     const uint64_t avoid = Z & ~low_mask();
     if (P.opt.zero_aware && avoid && buf.size() <= 4000) {
-      double best = sched_cost(sets, Z);
+      double best = sched_cost(sets, Z, &buf);
       std::vector<std::vector<uint64_t>> prefixes;
       for (const auto& c1 : avoiding(buf, avoid)) {
         if (c1.first == 0 || prefixes.size() >= 4) break;
@@ -699,7 +711,7 @@ struct Planner {
         const std::vector<uint64_t> tail = beam_sets(remaining);
         if (!remaining.empty() && tail.empty()) continue;
         alt.insert(alt.end(), tail.begin(), tail.end());
-        const double c = sched_cost(alt, Z);
+        const double c = sched_cost(alt, Z, &buf);
         if (c < best - 1e-9) {
           best = c;
           sets = alt;
@@ -945,6 +957,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "ctas_per_sm") ctas_per_sm = v;
   else if (key == "defer_gates") defer_gates = v;
   else if (key == "zero_aware") zero_aware = v;
+  else if (key == "zero_cost") zero_cost = v;
   else return false;
   return true;
 }
