@@ -675,7 +675,7 @@ struct Planner {
       double best = sched_cost(sets, Z, &buf);
       std::vector<std::vector<uint64_t>> prefixes;
       for (const auto& c1 : avoiding(buf, avoid)) {
-        if (c1.first == 0 || prefixes.size() >= 4) break;
+        if (c1.first == 0 || prefixes.size() >= (size_t)P.opt.zero_width) break;
         prefixes.push_back({c1.second});
       }
       // deeper prefixes: after each prefix, up to two more avoiding passes (zero_aware =
@@ -691,7 +691,7 @@ struct Planner {
           }
           int taken = 0;
           for (const auto& c2 : avoiding(remaining, avoid)) {
-            if (c2.first == 0 || taken >= 2) break;
+            if (c2.first == 0 || taken >= P.opt.zero_width / 2) break;
             std::vector<uint64_t> pre = prefixes[i];
             pre.push_back(c2.second);
             prefixes.push_back(pre);
@@ -958,6 +958,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "defer_gates") defer_gates = v;
   else if (key == "zero_aware") zero_aware = v;
   else if (key == "zero_cost") zero_cost = v;
+  else if (key == "zero_width") zero_width = v;
   else return false;
   return true;
 }
