@@ -242,3 +242,25 @@ def test_streaming_dynamic_final_states_vs_oracle(kind, params):
             continue
         assert keys[i] == r[0], i
         np.testing.assert_allclose(states[i].amps, r[1], atol=TOL["c128"], rtol=0)
+
+
+@pytest.mark.parametrize("kind,params", [
+    ("random", (17, 160, 11)), ("dyn", {"n": 18, "layers": 10, "every": 5, "nmeas": 3, "seed": 5}),
+])
+def test_known_zero_skipping_is_exact(kind, params):
+    """The known-zero machinery (items skipped, zeros generated in the gather instead of
+    read, the end-of-run zero store) computes exactly what the plain path computes: same
+    keys, equal amplitudes (context option zero_fill 1 vs 0, same plan)."""
+    k = workloads.random_dynamic(*params) if kind == "random" else workloads.dyn_circuit(**params)[1]
+    b = ir.bind(k, [])
+    ctx = _lib.context()
+    out = {}
+    for zf in (0, 1):
+        ctx.set_option("zero_fill", zf)
+        try:
+            out[zf] = sim.sample_final_states(b, 64, 7, 8)
+        finally:
+            ctx.set_option("zero_fill", 1)
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, c in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a.amps, c.amps)
