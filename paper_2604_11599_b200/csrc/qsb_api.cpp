@@ -58,9 +58,13 @@ namespace {
 
 size_t amp_bytes(int c64) { return c64 ? 8 : 16; }
 
-int tile_qubits(qsb_ctx ctx, int c64) {
+int tile_qubits(qsb_ctx ctx, int c64, bool staged = false) {
   if (ctx->opt_tile > 0) return (int)std::min<int64_t>(ctx->opt_tile, kMaxTile);
-  return 12;  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA
+  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA; complex128 passes whose
+  // gates are staged per slot (observe over parameter points) run 11-qubit tiles: 4 CTAs
+  // per SM hide the staging latency (VQE24 574 -> 616 points/s; DYN20 / RDC30, literal
+  // matrices, lose with 11)
+  return (staged && !c64) ? 11 : 12;
 }
 // contiguous low qubits of every tile: 3 (runs of 8 amplitudes: 128 B complex128, 64 B
 // complex64) by default -- measured on B200 with the beam-search tiling (round 2), the tile
@@ -1844,7 +1848,7 @@ int32_t qsb_observe(qsb_tape tp_in, int32_t precision, const double* params, int
   ctx->run_physical = false;
   RunTimer timer(ctx);
   PlanDev* pd;
-  int rc = get_plan(tp, c64, tile_qubits(ctx, c64), low_qubits(ctx, c64), reg_bits(ctx), &pd);
+  int rc = get_plan(tp, c64, tile_qubits(ctx, c64, t.has_param_angles), low_qubits(ctx, c64), reg_bits(ctx), &pd);
   if (rc) return rc;
   int64_t B = pick_batch(ctx, t, pd->plan, c64, npoints);
   QSB_CUDA(ctx->state.ensure((amp_bytes(c64) << t.n) * B));
