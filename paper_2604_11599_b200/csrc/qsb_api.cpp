@@ -628,9 +628,9 @@ int32_t qsb_ctx_set_option(qsb_ctx ctx, const char* key, int64_t value) {
   else if (k == "jit_min_qubits") ctx->opt_jit_min = value;
   else if (k == "dedup") ctx->opt_dedup = value;
   else if (k == "fuse") ctx->opt_fuse = value;
-  else if (k == "jit_async") ctx->opt_jit_async = value;
-  else if (k == "defer_copy") ctx->opt_defer_copy = value;
-  else if (k == "zero_fill") ctx->opt_zero_fill = value;  // first pass after a measurement: zero fill + kept items only  // dedup: branches read the old buffer in their first pass  // NVRTC in the background, generic kernel meanwhile
+  else if (k == "jit_async") ctx->opt_jit_async = value;    // NVRTC in the background, generic kernel meanwhile
+  else if (k == "defer_copy") ctx->opt_defer_copy = value;  // dedup: branches read the old buffer in their first pass
+  else if (k == "zero_fill") ctx->opt_zero_fill = value;    // known-zero amplitudes after a measurement stay lazy
   else if (k == "expval_low_qubits") ctx->opt_ev_lowq = value;  // contiguous run of the Pauli reducer's tiles
   else if (k == "expval_jit") ctx->opt_ev_jit = value;          // NVRTC-specialised Pauli reducer
   else if (k == "expval_jit_terms") ctx->opt_ev_jit_terms = value;  // its terms per launch (<= 32)

@@ -133,8 +133,8 @@ void launch_ctl_init(TrajCtl* ctl, uint64_t* bits, int nwords, uint32_t* guards,
 // their old representatives' buffers (StreamArgs::read_src = copy_src)
 void launch_dedup(const StreamArgs& a, int32_t* new_rep, int32_t* copy_src, int32_t* active, int32_t* nactive,
                   int c64, bool regroup, int32_t* split, cudaStream_t s);
-// zero the amplitudes the pending collapse rejects on the qubits M (first pass after a
-// measurement then runs only the kept items)
+// store the zeros of the amplitudes the pending collapse rejects on the qubits M (known-zero
+// amplitudes no pass has stored: end of a run, or before a pass that reads everything)
 void launch_zero_projected(const StreamArgs& a, int c64, uint64_t M, cudaStream_t s);
 // zero the states (+ epilogue partials) of the active slots before a tile-0-only init pass
 void launch_zero_slots(const StreamArgs& a, int c64, int zero_partials, cudaStream_t s);

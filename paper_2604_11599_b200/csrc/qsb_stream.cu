@@ -558,8 +558,8 @@ __global__ void k_accum_physical(const int32_t* nactive, double flops, double by
   phys[1] += flops * (double)*nactive;
 }
 
-// zero the state (and the epilogue partials) of the active slots: the init pass then
-// computes only the tile holding index 0 of each (PassDesc::init_zero == 2)
+// zero the state (and the epilogue partials) of the active slots: the passes from the
+// |0...0> start then run only the items not known to be zero (PassDesc::zero_tid)
 __global__ void k_zero_slots(StreamArgs a, int64_t amp_words, int zero_partials) {
   const int64_t n_act = a.active ? *a.nactive : a.slots;
   for (int64_t si = blockIdx.y; si < n_act; si += gridDim.y) {
@@ -576,8 +576,9 @@ __global__ void k_zero_slots(StreamArgs a, int64_t amp_words, int zero_partials)
   }
 }
 
-// the amplitudes the pending collapse rejects on the (out-of-tile) qubits M, per active
-// slot: zero stores, so that the next pass runs only the items the collapse keeps
+// the amplitudes the pending collapse rejects on the qubits M, per active slot: zero
+// stores of the known-zero amplitudes no pass has stored (end of a run, or before a pass
+// that reads every amplitude)
 __global__ void k_zero_projected(StreamArgs a, uint64_t M, int64_t amp_words, int amps_per_word) {
   const int64_t n_act = a.active ? *a.nactive : a.slots;
   for (int64_t si = blockIdx.y; si < n_act; si += gridDim.y) {
