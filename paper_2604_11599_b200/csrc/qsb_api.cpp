@@ -60,11 +60,13 @@ size_t amp_bytes(int c64) { return c64 ? 8 : 16; }
 
 int tile_qubits(qsb_ctx ctx, int c64, bool staged = false) {
   if (ctx->opt_tile > 0) return (int)std::min<int64_t>(ctx->opt_tile, kMaxTile);
-  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA; complex128 passes whose
-  // gates are staged per slot (observe over parameter points) run 11-qubit tiles: 4 CTAs
-  // per SM hide the staging latency (VQE24 574 -> 616 points/s; DYN20 / RDC30, literal
-  // matrices, lose with 11)
-  return (staged && !c64) ? 11 : 12;
+  // 64 KiB (complex128) / 32 KiB (complex64) of amplitudes per CTA.  (11-qubit tiles for
+  // complex128 observe passes -- 4 CTAs per SM for the per-slot gate staging -- won 7 % on
+  // VQE24 until the |0...0>-start planning (init_aware) made the 12-qubit plan mostly
+  // known-zero passes: 844 vs 639 points/s with 12.)
+  (void)staged;
+  (void)c64;
+  return 12;
 }
 // contiguous low qubits of every tile: 3 (runs of 8 amplitudes: 128 B complex128, 64 B
 // complex64) by default -- measured on B200 with the beam-search tiling (round 2), the tile

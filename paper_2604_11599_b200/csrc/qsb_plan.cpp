@@ -659,6 +659,63 @@ struct Planner {
     return c1;
   }
 
+  // cost of a schedule of the region at the |0...0> start (qubits not yet in a tile are
+  // known zero; the epilogue pass, if any, runs every item)
+  double init_cost(const std::vector<uint64_t>& sets, bool has_epi) const {
+    const uint64_t all = (t.n >= 64) ? ~0ull : ((1ull << t.n) - 1);
+    uint64_t Z = all;
+    double c = 0;
+    for (size_t i = 0; i < sets.size(); ++i) {
+      const bool epi = has_epi && i + 1 == sets.size();
+      c += epi ? 1.0 : std::ldexp(1.0, -popc(Z & ~sets[i]));
+      Z &= ~sets[i];
+    }
+    return c;
+  }
+
+  void init_prefix_search(const std::vector<int>& buf, bool has_epi, std::vector<uint64_t>& sets) const {
+    double best = init_cost(sets, has_epi);
+    struct Pre {
+      std::vector<uint64_t> sets;
+      std::vector<int> remaining;
+      uint64_t seen;
+    };
+    std::vector<Pre> level{Pre{{}, buf, 0}};
+    for (int depth = 0; depth < P.opt.init_aware + 1; ++depth) {
+      std::vector<Pre> next;
+      for (const Pre& pr : level) {
+        auto cands = candidates(pr.remaining);
+        int taken = 0;
+        for (const auto& c : cands) {
+          if (taken >= 3) break;
+          // after the first pass: at most 6 qubits new to the tiles so far
+          if (depth > 0 && popc(c.second & ~pr.seen) > 6) continue;
+          Pre np;
+          np.sets = pr.sets;
+          np.sets.push_back(c.second);
+          uint64_t S = c.second;
+          std::vector<int> chosen;
+          absorb(pr.remaining, S, false, &chosen, &np.remaining);
+          if (chosen.empty()) continue;
+          np.seen = pr.seen | c.second;
+          ++taken;
+          std::vector<uint64_t> alt = np.sets;
+          const std::vector<uint64_t> tail = beam_sets(np.remaining);
+          if (np.remaining.empty() || !tail.empty()) {
+            alt.insert(alt.end(), tail.begin(), tail.end());
+            const double cost = init_cost(alt, has_epi);
+            if (cost < best - 1e-9) {
+              best = cost;
+              sets = alt;
+            }
+          }
+          if (!np.remaining.empty()) next.push_back(std::move(np));
+        }
+      }
+      level.swap(next);
+    }
+  }
+
   void flush(std::vector<int>& buf, int epi_region) {
     const uint64_t Z = zero_next_;
     zero_next_ = 0;
@@ -667,6 +724,11 @@ struct Planner {
       return;
     }
     std::vector<uint64_t> sets = beam_sets(buf);
+    // the region at the |0...0> start: qubits no tile has held yet are still |0>, so a pass
+    // runs 2^-u of its items (u = such qubits outside its tile; §4.2 known-zero items).
+    // Also try schedules whose first passes add few new qubits at a time, the rest by the
+    // beam search; keep the cheapest
+    if (P.opt.init_aware && P.passes.empty() && !Z && buf.size() <= 4000) init_prefix_search(buf, epi_region >= 0, sets);
     // after a measurement: also try one or two first passes whose tiles avoid the projected
     // qubits (above the always-present low run), the rest by the beam search; keep the
     // cheapest schedule
@@ -959,6 +1021,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "zero_aware") zero_aware = v;
   else if (key == "zero_cost") zero_cost = v;
   else if (key == "zero_width") zero_width = v;
+  else if (key == "init_aware") init_aware = v;
   else return false;
   return true;
 }
