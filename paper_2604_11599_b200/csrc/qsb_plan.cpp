@@ -582,11 +582,12 @@ struct Planner {
   // tile sets of the passes of `buf` by a beam search over the tile set of each pass (kBeam
   // partial schedules, kCand tile sets tried per step, ranked by the gates still left):
   // the fewest passes found -- each pass is a full read + write of every state
-  std::vector<uint64_t> beam_sets(const std::vector<int>& buf) const {
+  std::vector<uint64_t> beam_sets(const std::vector<int>& buf, int max_beam = 64) const {
     if (buf.empty()) return {};
     // beam width scaled to the region so planning stays ~linear in the gate count (64 x 16
     // up to ~6k gates per region: DYN20 / RDC / VQE; a 100k-gate static region gets 4 x 8)
-    const int kBeam = (int)std::max<size_t>(4, std::min<size_t>(64, 400000 / std::max<size_t>(1, buf.size())));
+    const int kBeam = (int)std::max<size_t>(
+        4, std::min<size_t>((size_t)max_beam, 400000 / std::max<size_t>(1, buf.size())));
     const int kCand = kBeam >= 16 ? 16 : 8;
     struct Sched {
       std::vector<uint64_t> sets;
@@ -659,6 +660,11 @@ struct Planner {
     return c1;
   }
 
+  // beam width of the tails the zero-aware searches evaluate: full for small regions,
+  // narrower for large ones so that planning stays ~1-2 s on RDC30 (a tail is adopted only
+  // when its schedule is cheaper than the full-width default)
+  static int tail_beam(size_t gates) { return gates <= 700 ? 64 : 8; }
+
   // cost of a schedule of the region at the |0...0> start (qubits not yet in a tile are
   // known zero; the epilogue pass, if any, runs every item)
   double init_cost(const std::vector<uint64_t>& sets, bool has_epi) const {
@@ -700,7 +706,7 @@ struct Planner {
           np.seen = pr.seen | c.second;
           ++taken;
           std::vector<uint64_t> alt = np.sets;
-          const std::vector<uint64_t> tail = beam_sets(np.remaining);
+          const std::vector<uint64_t> tail = beam_sets(np.remaining, tail_beam(buf.size()));
           if (np.remaining.empty() || !tail.empty()) {
             alt.insert(alt.end(), tail.begin(), tail.end());
             const double cost = init_cost(alt, has_epi);
@@ -770,7 +776,7 @@ struct Planner {
           remaining.swap(rest);
         }
         std::vector<uint64_t> alt = pre;
-        const std::vector<uint64_t> tail = beam_sets(remaining);
+        const std::vector<uint64_t> tail = beam_sets(remaining, tail_beam(buf.size()));
         if (!remaining.empty() && tail.empty()) continue;
         alt.insert(alt.end(), tail.begin(), tail.end());
         const double c = sched_cost(alt, Z, &buf);
