@@ -665,37 +665,38 @@ struct Planner {
   // when its schedule is cheaper than the full-width default)
   static int tail_beam(size_t gates) { return gates <= 700 ? 64 : 8; }
 
-  // cost of a schedule of the region at the |0...0> start (qubits not yet in a tile are
-  // known zero; the epilogue pass, if any, runs every item)
-  double init_cost(const std::vector<uint64_t>& sets, bool has_epi) const {
+  // prefixes of up to `depth` passes, each from the ordinary candidates but adding at most
+  // `max_new` known-zero qubits (of Z, not yet in a tile of the prefix; the first pass of
+  // the |0...0> start is free), the rest by the beam search; keep the cheapest schedule
+  void prefix_search(const std::vector<int>& buf, uint64_t Z, bool has_epi, int depth_max, int max_new,
+                     std::vector<uint64_t>& sets) const {
+    auto cost_of = [&](const std::vector<uint64_t>& ss) {
+      uint64_t z = Z;
+      double c = 0;
+      for (size_t i = 0; i < ss.size(); ++i) {
+        const bool epi = has_epi && i + 1 == ss.size();
+        c += epi ? 1.0 : std::ldexp(1.0, -popc(z & ~ss[i]));
+        z &= ~ss[i];
+      }
+      return c;
+    };
+    double best = cost_of(sets);
     const uint64_t all = (t.n >= 64) ? ~0ull : ((1ull << t.n) - 1);
-    uint64_t Z = all;
-    double c = 0;
-    for (size_t i = 0; i < sets.size(); ++i) {
-      const bool epi = has_epi && i + 1 == sets.size();
-      c += epi ? 1.0 : std::ldexp(1.0, -popc(Z & ~sets[i]));
-      Z &= ~sets[i];
-    }
-    return c;
-  }
-
-  void init_prefix_search(const std::vector<int>& buf, bool has_epi, std::vector<uint64_t>& sets) const {
-    double best = init_cost(sets, has_epi);
+    const bool init = Z == all;
     struct Pre {
       std::vector<uint64_t> sets;
       std::vector<int> remaining;
       uint64_t seen;
     };
     std::vector<Pre> level{Pre{{}, buf, 0}};
-    for (int depth = 0; depth < P.opt.init_aware + 1; ++depth) {
+    for (int depth = 0; depth < depth_max; ++depth) {
       std::vector<Pre> next;
       for (const Pre& pr : level) {
         auto cands = candidates(pr.remaining);
         int taken = 0;
         for (const auto& c : cands) {
           if (taken >= 3) break;
-          // after the first pass: at most 6 qubits new to the tiles so far
-          if (depth > 0 && popc(c.second & ~pr.seen) > 6) continue;
+          if (!(init && depth == 0) && popc(c.second & Z & ~pr.seen & ~low_mask()) > max_new) continue;
           Pre np;
           np.sets = pr.sets;
           np.sets.push_back(c.second);
@@ -709,7 +710,7 @@ struct Planner {
           const std::vector<uint64_t> tail = beam_sets(np.remaining, tail_beam(buf.size()));
           if (np.remaining.empty() || !tail.empty()) {
             alt.insert(alt.end(), tail.begin(), tail.end());
-            const double cost = init_cost(alt, has_epi);
+            const double cost = cost_of(alt);
             if (cost < best - 1e-9) {
               best = cost;
               sets = alt;
@@ -720,6 +721,11 @@ struct Planner {
       }
       level.swap(next);
     }
+  }
+
+  void init_prefix_search(const std::vector<int>& buf, bool has_epi, std::vector<uint64_t>& sets) const {
+    const uint64_t all = (t.n >= 64) ? ~0ull : ((1ull << t.n) - 1);
+    prefix_search(buf, all, has_epi, P.opt.init_aware + 1, 6, sets);
   }
 
   void flush(std::vector<int>& buf, int epi_region) {
@@ -786,6 +792,9 @@ struct Planner {
         }
       }
     }
+    // after a measurement, prefixes that take in the projected qubits one or two at a time
+    if (P.opt.zero_step > 0 && avoid && buf.size() <= 4000)
+      prefix_search(buf, avoid, epi_region >= 0, 3, P.opt.zero_step, sets);
     // replay the chosen tile sets
     std::vector<int> remaining = buf;
     for (size_t i = 0; i < sets.size(); ++i) {
@@ -1028,6 +1037,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "zero_cost") zero_cost = v;
   else if (key == "zero_width") zero_width = v;
   else if (key == "init_aware") init_aware = v;
+  else if (key == "zero_step") zero_step = v;
   else return false;
   return true;
 }
