@@ -631,7 +631,7 @@ struct Planner {
     for (size_t i = 0; i < sets.size(); ++i) {
       const bool epi = i + 1 == sets.size();
       double w = 1.0;
-      if (buf && P.opt.zero_cost) {
+      if (buf && (P.opt.zero_cost == 1 || P.opt.zero_cost == 3)) {
         uint64_t S = sets[i];
         std::vector<int> chosen, rest;
         absorb(remaining, S, false, &chosen, &rest);
@@ -665,6 +665,17 @@ struct Planner {
   // when its schedule is cheaper than the full-width default)
   static int tail_beam(size_t gates) { return gates <= 700 ? 64 : 8; }
 
+  // compute weight of a pass's gates in dense-1q-gate units (a dense gate 1, a diagonal
+  // 0.3, a permutation 0.1): the gate-weighted cost model's numerator
+  double gate_work(const std::vector<int>& gates) const {
+    double w = 0;
+    for (int gi : gates) {
+      const DevOp& d = t.dev[gi];
+      w += d.gclass == GC_DENSE ? 1.0 : d.gclass == GC_DIAG ? 0.3 : 0.1;
+    }
+    return w;
+  }
+
   // prefixes of up to `depth` passes, each from the ordinary candidates but adding at most
   // `max_new` known-zero qubits (of Z, not yet in a tile of the prefix; the first pass of
   // the |0...0> start is free), the rest by the beam search; keep the cheapest schedule
@@ -673,9 +684,18 @@ struct Planner {
     auto cost_of = [&](const std::vector<uint64_t>& ss) {
       uint64_t z = Z;
       double c = 0;
+      std::vector<int> remaining = buf;
       for (size_t i = 0; i < ss.size(); ++i) {
         const bool epi = has_epi && i + 1 == ss.size();
-        c += epi ? 1.0 : std::ldexp(1.0, -popc(z & ~ss[i]));
+        double w = 1.0;
+        if (P.opt.zero_cost == 1 || P.opt.zero_cost == 2) {  // gate-weighted: max(memory floor, gates x per-gate compute)
+          uint64_t S = ss[i];
+          std::vector<int> chosen, rest;
+          absorb(remaining, S, false, &chosen, &rest);
+          remaining.swap(rest);
+          w = std::max(0.45, gate_work(chosen) / 70.0);
+        }
+        c += w * (epi ? 1.0 : std::ldexp(1.0, -popc(z & ~ss[i])));
         z &= ~ss[i];
       }
       return c;

@@ -55,7 +55,7 @@ struct EngineOptions {
   int ctas_per_sm = 0;        // cap of the persistent pass grid per SM (0: occupancy)
   int defer_gates = 0;        // gates commuting with a measurement region run after it (measured slower: off)
   int zero_aware = 2;         // after a measurement, the first (1) or first two (2) passes may avoid the projected qubits
-  int zero_cost = 0;          // their cost model: 0 = 1 per full pass, 1 = gate-weighted
+  int zero_cost = 2;          // their cost model: 0 = 1 per full pass; gate-weighted 1 = everywhere, 2 = prefix searches, 3 = zero_aware only
   int zero_width = 4;         // first-pass candidates tried (and width / 2 per later avoiding pass)
   int zero_step = 1;          // after a measurement: also prefixes taking in <= zero_step projected qubits per pass
   int init_aware = 2;         // the region at the |0...0> start: prefixes of up to init_aware + 1 passes by known-zero cost
