@@ -814,7 +814,7 @@ struct Planner {
     }
     // after a measurement, prefixes that take in the projected qubits one or two at a time
     if (P.opt.zero_step > 0 && avoid && buf.size() <= 4000)
-      prefix_search(buf, avoid, epi_region >= 0, 3, P.opt.zero_step, sets);
+      prefix_search(buf, avoid, epi_region >= 0, P.opt.zero_depth, P.opt.zero_step, sets);
     // replay the chosen tile sets
     std::vector<int> remaining = buf;
     for (size_t i = 0; i < sets.size(); ++i) {
@@ -1058,6 +1058,7 @@ bool EngineOptions::set(const std::string& key, int64_t value) {
   else if (key == "zero_width") zero_width = v;
   else if (key == "init_aware") init_aware = v;
   else if (key == "zero_step") zero_step = v;
+  else if (key == "zero_depth") zero_depth = v;
   else return false;
   return true;
 }

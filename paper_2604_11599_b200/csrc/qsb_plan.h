@@ -57,12 +57,13 @@ struct EngineOptions {
   int zero_aware = 2;         // after a measurement, the first (1) or first two (2) passes may avoid the projected qubits
   int zero_cost = 2;          // their cost model: 0 = 1 per full pass; gate-weighted 1 = everywhere, 2 = prefix searches, 3 = zero_aware only
   int zero_width = 4;         // first-pass candidates tried (and width / 2 per later avoiding pass)
+  int zero_depth = 3;         // ... prefixes of up to zero_depth passes
   int zero_step = 1;          // after a measurement: also prefixes taking in <= zero_step projected qubits per pass
   int init_aware = 2;         // the region at the |0...0> start: prefixes of up to init_aware + 1 passes by known-zero cost
   uint64_t key() const {
     const int v[] = {pair_aware, phase_search, block_condx, inline_phases, inline_min_gates, ffma2, packed_gates,
                      last_direct, last_direct_maxlow, minblocks, edge_x, ctas_per_sm, defer_gates, inline_max_phases,
-                     zero_aware, zero_cost, zero_width, init_aware, zero_step};
+                     zero_aware, zero_cost, zero_width, init_aware, zero_step, zero_depth};
     uint64_t h = 1469598103934665603ull;
     for (int x : v) h = (h ^ (uint64_t)(uint32_t)x) * 1099511628211ull;
     return h;
