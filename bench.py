@@ -369,7 +369,10 @@ def run_ours(args) -> None:
                          "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": traffic,
                          "kernel": "k_pass (fused gate pass)", "peak_kind": which,
                          "algorithmic_bytes_per_step": pass_bytes / args.steps,
-                         "pass_ms_per_step": pass_ms / args.steps},
+                         "pass_ms_per_step": pass_ms / args.steps,
+                         "note": "bytes the passes must move: amplitudes known to be zero (untouched "
+                                 "qubits, rejected by the last collapse) are neither read nor stored; "
+                                 "the binding roof of the complex128 passes is FP64 (compute_roofline)"},
             # the pass kernel's binding roof for complex128 is the FP64 FMA pipe, not HBM:
             # executed floating-point work (FMA = 2) vs the FMA throughput probed on this GPU
             "compute_roofline": {"bound": "fp64" if prec == "c128" else "fp32",
